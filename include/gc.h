@@ -1,0 +1,181 @@
+/*
+ * include/gc.h -- C ABI of libgc.so, the B200 (sm_100a) greedy binary-code engine.
+ *
+ * The operation (PAPER.md = arXiv 1507.05398 text, /root/reference/PAPER.md):
+ *   "Given n, d ... construct the code C using different orderings in greedy
+ *    approach" (Sec. 3).  "First step is ordering all the vectors of
+ *    F_2^n.  Next, the vectors are appended to code C from the set F_2^n one by one
+ *    starting from zero vector.  The vectors are checked to satisfy the constraint
+ *    of minimum Hamming distance d from all the previous choices in code C.  The
+ *    algorithm terminates when all the 2^n vectors are exhausted."
+ *   Distance = popcount(u XOR v) (Sec. 5.2).  Orderings: lexicographic,
+ *   Gray, graded-lexicographic, graded-reverse-lexicographic (Sec. 4.2).
+ *
+ * Vector encoding (reading R4): a vector of F_2^n is the unsigned integer
+ * whose bit n-1-i holds coordinate i, so lexicographic order is ascending integers
+ * (PAPER.md:89 lists {000, 001, ..., 111}).  Orderings (R1, R2):
+ *   GC_LEX            rank r -> r
+ *   GC_GRAY           rank r -> r ^ (r >> 1)            (binary reflected Gray code)
+ *   GC_GRADED_LEX     weight ascending, then value ascending
+ *   GC_GRADED_REVLEX  weight ascending, then value descending
+ * Every ordering starts at the zero vector (rank 0).
+ *
+ * Result: the greedy code in ACCEPTANCE order (= increasing rank).  It is a pure
+ * function of (n, d, ordering): no option below changes it (PAPER.md:159's
+ * "selective kernel launch" and every other schedule only reorder the evaluation
+ * of "distance >= d for all previous choices").
+ *
+ * Conventions for every entry point:
+ *   - return value is a gc_status; no exception or signal crosses the ABI;
+ *   - argument validation happens before any CUDA call (so it is testable
+ *     without a GPU) and leaves outputs untouched on error;
+ *   - gc_last_error() returns a thread-local message for the last failure;
+ *   - one construction per device at a time (calls on one device serialise on an
+ *     internal per-device context; the library owns its scratch device memory).
+ */
+#ifndef GC_H_
+#define GC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GC_ABI_VERSION 1
+
+typedef enum gc_ordering {
+    GC_LEX = 0,            /* lexicographic                        */
+    GC_GRAY = 1,           /* Gray order, reflected binary (R1)      */
+    GC_GRADED_LEX = 2,     /* graded-lexicographic (R2)              */
+    GC_GRADED_REVLEX = 3   /* graded-reverse-lexicographic (R2)      */
+} gc_ordering;
+
+typedef enum gc_status {
+    GC_OK = 0,
+    GC_EINVAL = 1,         /* invalid argument (NULL pointer, n == 0, d == 0, d > n, bad ordering, bad option) */
+    GC_ERANGE = 2,         /* rank or vector out of [0, 2^n)                                                      */
+    GC_ENOSPC = 3,         /* output capacity too small; *out_count receives the required size                    */
+    GC_EUNSUPPORTED = 4,   /* n > 32 on the GPU path (device words are 32-bit)                                    */
+    GC_ECUDA = 5,          /* CUDA runtime / launch error (no device, kernel fault, ...)                           */
+    GC_ENOMEM = 6,         /* device or pinned host allocation failed                                              */
+    GC_ENCCL = 7,          /* NCCL unavailable or a collective failed (multi-process entry points)                 */
+    GC_EINTERNAL = 8       /* internal consistency check failed (a bug; please report)                             */
+} gc_status;
+
+/* Schedule knobs.  None of them changes the result.  Zero-initialise and set
+ * struct_size = sizeof(gc_options); a zero field means "default". */
+typedef struct gc_options {
+    uint32_t struct_size;
+    uint32_t tile_min;       /* smallest candidate tile K (power of 2, >= 32), default 256              */
+    uint32_t tile_max;       /* largest candidate tile K (power of 2, <= 2^20), default 65536           */
+    uint32_t window0;        /* first newest-first codebook window (power of 2), default 1024           */
+    uint32_t emulate_ranks;  /* >1: split every tile's candidates into this many partitions on ONE GPU,
+                                exactly as gc_generate_rank splits them across GPUs (testing), default 1 */
+    uint32_t flags;          /* GC_FLAG_* below                                                          */
+} gc_options;
+
+#define GC_FLAG_NO_EARLY_EXIT  0x1u  /* screen every candidate against the whole codebook, one phase     */
+#define GC_FLAG_SYNC_TILES     0x2u  /* host waits after every tile (debugging)                         */
+#define GC_FLAG_FORCE_SEQ_RESOLVE 0x4u /* in-tile resolve by the sequential fallback (testing)           */
+
+/* Counters of one construction (filled when a gc_stats* is passed). */
+typedef struct gc_stats {
+    uint32_t struct_size;
+    uint32_t n_ranks;        /* world size used (1, or emulate_ranks / world)                       */
+    double device_ms;        /* device time between the first and the last kernel (CUDA events)       */
+    double wall_ms;          /* host wall time of the call                                            */
+    uint64_t M;              /* codewords produced                                                    */
+    uint64_t tiles;          /* candidate tiles                                                       */
+    uint64_t phases;         /* screen phases launched                                                */
+    uint64_t checks_exec;    /* candidate-codeword distance evaluations executed by the screen (lane work) */
+    uint64_t survivors;      /* candidates that passed the screen (sum over tiles)                    */
+    uint64_t conflicts;      /* in-tile survivor pairs at distance < d (sum over tiles)                */
+    uint64_t resolve_checks; /* survivor-survivor distance evaluations in the in-tile resolve         */
+    double w_def;            /* definitional work sum_j (2^n - 1 - rank_j): every candidate against
+                                every codeword accepted before it                       */
+} gc_stats;
+
+/* ------------------------------------------------------------------ generate */
+
+/* The greedy code for (n, d, ordering) on the current CUDA device.
+ *   n in [1, 32] on the GPU (GC_EUNSUPPORTED above), d in [1, n].
+ *   out_codewords: caller-owned HOST buffer of *out_count elements (may be NULL iff *out_count == 0).
+ *   in: *out_count = capacity; out: GC_OK -> *out_count = M and out_codewords[0..M) in acceptance order;
+ *   GC_ENOSPC -> *out_count = M (required capacity), buffer contents unspecified.
+ * gc_capacity_bound(n, d) elements always suffice. */
+int gc_generate(uint32_t n, uint32_t d, gc_ordering ordering,
+                uint64_t *out_codewords, uint64_t *out_count);
+
+/* As gc_generate, with schedule options (NULL = defaults) and optional stats (NULL = none). */
+int gc_generate_ex(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt,
+                   uint64_t *out_codewords, uint64_t *out_count, gc_stats *stats);
+
+/* Device-buffer variant for callers that own device memory and streams (PyTorch):
+ *   d_codebook: DEVICE buffer of `capacity` uint32 words (the code, acceptance order);
+ *   d_count:    DEVICE uint64 receiving M;  stream: cudaStream_t (NULL = legacy default stream).
+ * Work is enqueued on `stream`.  With stats == NULL the call returns once everything is
+ * enqueued (results valid when the stream reaches this point; device scratch stays owned
+ * by the library and is reused by the next call on this device, which must be ordered
+ * after this one -- e.g. the same stream).  With stats != NULL the call synchronises the
+ * stream and fills *stats.  If M would exceed capacity the device error flag is set and a
+ * later synchronising call reports GC_ENOSPC.  capacity >= gc_capacity_bound(n, d) is safe. */
+int gc_generate_device(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt,
+                       uint32_t *d_codebook, uint64_t capacity, uint64_t *d_count,
+                       void *stream, gc_stats *stats);
+
+/* Upper bound on M: the sphere-packing (Hamming) bound for (n, d); for even d the
+ * bound of (n-1, d-1) (a code of even distance d and length n punctures to one of
+ * length n-1 and distance d-1).  Clamped to 2^n.  Returns 0 if the arguments are invalid.
+ * (28,3) -> 9,256,395; (26,4) -> 1,290,555; (24,8) -> 4,096. */
+uint64_t gc_capacity_bound(uint32_t n, uint32_t d);
+
+/* ---------------------------------------------------------- orderings (host) */
+
+/* rank -> vector in `ordering`.  n in [1, 63]; GC_ERANGE if rank >= 2^n. */
+int gc_rank_to_vector(gc_ordering ordering, uint32_t n, uint64_t rank, uint64_t *out_vec);
+
+/* vector -> rank (inverse of gc_rank_to_vector).  GC_ERANGE if vec >= 2^n. */
+int gc_vector_to_rank(gc_ordering ordering, uint32_t n, uint64_t vec, uint64_t *out_rank);
+
+/* out[i] = gc_rank_to_vector(first + i), i < count, computed on the HOST. */
+int gc_ranks_to_vectors(gc_ordering ordering, uint32_t n, uint64_t first, uint64_t count,
+                        uint64_t *out);
+
+/* The same map evaluated by the DEVICE candidate generator the screen uses:
+ * d_out (DEVICE, count uint32) receives the vectors of ranks first .. first+count-1.
+ * n in [1, 32].  Synchronises `stream` (NULL = legacy default stream). */
+int gc_ranks_to_vectors_device(gc_ordering ordering, uint32_t n, uint64_t first, uint64_t count,
+                               uint32_t *d_out, void *stream);
+
+/* --------------------------------------------------------------- multi-GPU */
+
+/* Size in bytes of the NCCL unique id (128).  0 if NCCL cannot be loaded. */
+size_t gc_nccl_id_bytes(void);
+
+/* Fill id[0..gc_nccl_id_bytes()) with a fresh NCCL unique id (call on one rank, broadcast
+ * the bytes to the others, e.g. over a torch.distributed process group).  GC_ENCCL if NCCL
+ * (libnccl.so.2, loaded at run time) is unavailable. */
+int gc_nccl_unique_id(uint8_t *id, size_t id_bytes);
+
+/* One rank of a `world`-GPU construction (one process per GPU, current device = this
+ * rank's GPU).  Every rank screens 1/world of each tile's candidates against its full
+ * (replicated) codebook; the survivor bit-masks are all-gathered with NCCL once per tile;
+ * every rank then resolves the tile identically, so all ranks end with the same code.
+ * Buffers/stream/stats as gc_generate_device; the call synchronises `stream`.
+ * world == 1 is allowed (no NCCL is used). */
+int gc_generate_rank(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt,
+                     int rank, int world, const uint8_t *nccl_id, size_t id_bytes,
+                     uint32_t *d_codebook, uint64_t capacity, uint64_t *d_count,
+                     void *stream, gc_stats *stats);
+
+/* ------------------------------------------------------------------- misc */
+const char *gc_strerror(int status);
+const char *gc_last_error(void);   /* thread-local detail of the last failure ("" if none) */
+int gc_abi_version(void);          /* GC_ABI_VERSION */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GC_H_ */

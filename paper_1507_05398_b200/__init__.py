@@ -1,0 +1,43 @@
+"""B200-native greedy binary-code construction (arXiv 1507.05398) -- Python binding.
+
+A thin ctypes layer over ``libgc.so`` (C ABI: ``include/gc.h``).  Every function
+here only marshals arguments; every step of the construction runs in the library's
+sm_100a kernels.  PyTorch is used only for device memory and streams (the
+``*_device`` / ``gc_generate_rank`` entry points take tensors).
+
+If ``libgc.so`` is missing this module raises ImportError -- there is no CPU
+fallback anywhere in the product path.
+"""
+from __future__ import annotations
+
+from ._binding import (  # noqa: F401
+    GC_FLAG_FORCE_SEQ_RESOLVE,
+    GC_FLAG_NO_EARLY_EXIT,
+    GC_FLAG_SYNC_TILES,
+    GC_GRADED_LEX,
+    GC_GRADED_REVLEX,
+    GC_GRAY,
+    GC_LEX,
+    ORDERINGS,
+    GCError,
+    LIB_PATH,
+    exported_symbols,
+    gc_abi_version,
+    gc_capacity_bound,
+    gc_generate,
+    gc_generate_device,
+    gc_generate_ex,
+    gc_generate_rank,
+    gc_last_error,
+    gc_nccl_id_bytes,
+    gc_nccl_unique_id,
+    gc_rank_to_vector,
+    gc_ranks_to_vectors,
+    gc_ranks_to_vectors_device,
+    gc_strerror,
+    gc_vector_to_rank,
+    ordering_id,
+)
+
+__all__ = [n for n in dir() if n.startswith("gc_") or n.startswith("GC_")] + [
+    "GCError", "ORDERINGS", "ordering_id", "LIB_PATH", "exported_symbols"]

@@ -1,0 +1,61 @@
+// gc_internal.h -- shared declarations between gc_abi.cpp (validation, host orderings,
+// NCCL loader) and gc_engine.cu (device kernels and the tile scheduler).
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/gc.h"
+
+namespace gc {
+
+// thread-local last-error message (gc_last_error)
+void set_error(const std::string &msg);
+void clear_error();
+
+// resolved schedule options (defaults applied, validated)
+struct Options {
+    uint32_t tile_min = 256;
+    uint32_t tile_max = 65536;
+    uint32_t window0 = 1024;
+    uint32_t emulate_ranks = 1;
+    uint32_t flags = 0;
+};
+int resolve_options(const gc_options *opt, Options *out);   // GC_OK / GC_EINVAL
+
+// ---- NCCL, loaded with dlopen at first use (no link-time dependency) ----
+struct NcclUid { char internal[128]; };   // layout of ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128)
+constexpr int kNcclUint32 = 3;             // ncclDataType_t ncclUint32
+struct NcclApi {
+    bool ok = false;
+    size_t id_bytes = 128;
+    int (*GetUniqueId)(NcclUid *uid) = nullptr;
+    int (*CommInitRank)(void **comm, int nranks, NcclUid id, int rank) = nullptr;
+    int (*AllGather)(const void *send, void *recv, size_t count, int dtype, void *comm, void *stream) = nullptr;
+    int (*CommDestroy)(void *comm) = nullptr;
+    const char *(*GetErrorString)(int) = nullptr;
+};
+const NcclApi *nccl_api();   // nullptr if libnccl.so.2 cannot be loaded
+int nccl_comm_init(void **comm, int world, int rank, const uint8_t *id, size_t id_bytes);  // GC_OK/GC_ENCCL
+int nccl_allgather_u32(const uint32_t *send, uint32_t *recv, size_t count_per_rank, void *comm, void *stream);
+void nccl_comm_destroy(void *comm);
+
+// ---- engine (gc_engine.cu) ----
+struct RunArgs {
+    uint32_t n, d;
+    int ordering;
+    Options opt;
+    int rank = 0, world = 1;
+    void *nccl_comm = nullptr;      // world > 1
+    uint32_t *d_codebook = nullptr; // device, capacity words
+    uint64_t capacity = 0;
+    uint64_t *d_count = nullptr;    // device
+    void *stream = nullptr;
+    gc_stats *stats = nullptr;      // non-null -> synchronise and fill
+};
+int engine_run(const RunArgs &a);
+int engine_ranks_to_vectors_device(int ordering, uint32_t n, uint64_t first, uint64_t count,
+                                   uint32_t *d_out, void *stream);
+
+}  // namespace gc
