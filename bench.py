@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""bench.py -- one JSON line for the greedy binary-code construction on B200.
+
+A STEP is one whole construction (every row of SURVEY.md Sec. 8(a): candidate
+generation, windowed screen, in-tile resolve, commit) for the workload
+(n, d, ordering).  Default workload: n=28, d=3, lexicographic (BASELINE.json
+configs[4], the config BASELINE's metric is quoted on at 1/2/4/8 GPUs).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload 28,3,lex] [--impl b200|reference]
+
+metric: candidate-codeword distance checks per second, counted DEFINITIONALLY as the
+paper's kernel performs them (every candidate against every codeword accepted before it,
+PAPER.md:73): W_def = sum_j (2^n - 1 - rank_j).  value = W_def / (device time per step).
+ms_per_step is the wall (device) time of one construction.  The executed checks
+(W_exec, after early exit) and the POPC-pipe roofline of the screen kernel are reported
+beside it.
+
+N > 1: launched by torch.distributed.run, one process per GPU; each rank screens 1/N of
+every tile (gc_generate_rank over an NCCL communicator).  Strong scaling: the same
+construction at every N.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+POPC_PER_CLK_PER_SM = 16     # measured: profiles/r01_popc_peak.txt (15.35 at the held clock)
+
+
+def parse_workload(s: str):
+    n, d, o = s.split(",")
+    return int(n), int(d), o
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                clk, mx, util = float(r[1]), float(r[2]), float(r[9])
+            except Exception:
+                continue
+            smax = mx
+            if util > 0:
+                sm.append(clk)
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(self.rows), "samples_under_load": len(sm)}
+
+
+def load_traffic():
+    """dram bytes per screen launch from the committed ncu --set full summary (or None)."""
+    p = os.path.join(ROOT, "profiles", "screen_ncu_summary.json")
+    try:
+        return json.load(open(p)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU oracle
+
+def oracle_sample(n, d, ordering, budget_s=20.0, start_log2=16):
+    """The oracle (O1, plain serial greedy, Fig. 2(a)) as it stands, on a
+    bounded PREFIX of the same workload's scan: the first 2^k ranks, k grown until the
+    budget is used.  Returns (W_def of the prefix / seconds, description)."""
+    import numpy as np
+    import oracle as O
+    best = None
+    k = min(start_log2, n)
+    spent = 0.0
+    while True:
+        nranks = 1 << k
+        if ordering in ("lex", "gray"):
+            # the first 2^k ranks of the n-bit lex / reflected Gray order are the k-bit order
+            table = O.order_table(ordering, k)
+        else:
+            table = O.order_table(ordering, n)[:nranks].copy()
+        t = time.perf_counter()
+        w = O.greedy_plain(n, d, ordering, nranks=nranks, table=table)
+        dt = time.perf_counter() - t
+        spent += dt
+        # ranks of accepted words in the prefix: position in the table
+        pos = np.searchsorted(np.sort(table), w)
+        inv = np.argsort(table)
+        ranks = inv[pos]
+        wdef = int((nranks - 1 - ranks.astype(np.int64)).sum())
+        best = (wdef / dt, f"O1 on ranks [0, 2^{k}) of ({n},{d},{ordering}): M={len(w)}, "
+                           f"W_def={wdef:.4g} checks in {dt:.2f} s, 1 thread")
+        if spent + 4 * dt > budget_s or k >= n:
+            return best
+        k += 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n, d, o = parse_workload(args.workload)
+    import numpy as np
+    import oracle as O
+    k = min(args.ref_log2, n)
+    nranks = 1 << k
+    table = O.order_table(o, k) if o in ("lex", "gray") else O.order_table(o, n)[:nranks].copy()
+    inv = np.argsort(table)
+    srt = np.sort(table)
+
+    def step():
+        t = time.perf_counter()
+        w = O.greedy_plain(n, d, o, nranks=nranks, table=table)
+        dt = time.perf_counter() - t
+        ranks = inv[np.searchsorted(srt, w)]
+        return dt, int((nranks - 1 - ranks.astype(np.int64)).sum())
+
+    for _ in range(args.warmup):
+        step()
+    tot, wdef = 0.0, 0
+    for _ in range(args.steps):
+        dt, wd = step()
+        tot += dt
+        wdef += wd
+    val = wdef / tot
+    sample = f"O1 (oracle/, plain serial greedy) on ranks [0, 2^{k}) of ({n},{d},{o}) per step, 1 thread"
+    line = {
+        "impl": "reference", "metric": "candidate-codeword distance checks/sec (definitional W_def)",
+        "value": val, "unit": "checks/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (the whole space F_2^n, no dataset)",
+        "config": {"workload": f"n={n},d={d},{o}", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "checks/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "checks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ B200 arm
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1507_05398_b200 as gc
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world:
+        print(f"--gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n, d, o = parse_workload(args.workload)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(gc.gc_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        comm = gc.gc_comm_create(bytes(idt.cpu().numpy().tobytes()), rank, world)
+    else:
+        comm = gc.gc_comm_create(None, 0, 1)
+
+    cap = gc.gc_capacity_bound(n, d)
+    codebook = torch.empty(cap, dtype=torch.int32, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    opts = {"flags": gc.GC_FLAG_KERNEL_TIMING}
+
+    def construct():
+        return gc.gc_generate_rank(n, d, o, comm, codebook, count, stream=stream, options=opts)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        construct()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    stats = []
+    dev_ms = 0.0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.zero_()                      # L2 flushed between timed steps (outside the events)
+        ev[k][0].record(stream)
+        st = construct()                   # synchronises the stream at the end
+        ev[k][1].record(stream)
+        stats.append(st)
+    barrier()
+    sampler.stop()
+    dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    ms_per_step = max_ms / args.steps
+    M = int(count.item())
+    w_def = stats[-1]["w_def"]
+    value = w_def / (ms_per_step * 1e-3)
+
+    # e2e through the public API: host buffers, device->host copy of the code inside the region
+    e2e_val, d2h = None, 0
+    if world == 1:
+        gc.gc_generate(n, d, o)       # warm (allocations)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ds = torch.cuda.default_stream(dev)
+        tot = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            e0.record(ds)
+            w = gc.gc_generate(n, d, o)
+            e1.record(ds)
+            torch.cuda.synchronize(dev)
+            tot += e0.elapsed_time(e1)
+            d2h = w.nbytes
+        e2e_val = w_def / (tot / args.steps * 1e-3)
+    else:
+        # each rank constructs; rank 0 reads the code back to the host
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            e0.record(stream)
+            construct()
+            host = codebook[:M].cpu() if rank == 0 else None
+            e1.record(stream)
+            barrier()
+            tot += e0.elapsed_time(e1)
+            if rank == 0:
+                d2h = host.numel() * 4 + 8
+        tt = torch.tensor([tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_val = w_def / (float(tt.item()) / args.steps * 1e-3)
+
+    # roofline of the dominant kernel (k_screen): executed checks / its summed device time
+    checks = sum(s["checks_exec"] for s in stats)
+    screen_ms = sum(s["screen_ms"] for s in stats)
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz") or 1965.0)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = sms * POPC_PER_CLK_PER_SM * sm_max * 1e6
+    achieved = checks / (screen_ms * 1e-3) if screen_ms > 0 else 0.0
+    clocks = sampler.summary()
+
+    if rank == 0:
+        line = {
+            "metric": "candidate-codeword distance checks/sec (definitional W_def)",
+            "value": value, "unit": "checks/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (the whole space F_2^n in the chosen ordering; no dataset)",
+            "config": {"workload": f"n={n},d={d},{o}", "M": M, "w_def": w_def,
+                       "parallelism": f"candidate-partitioned x{world}, replicated codebook",
+                       "l2": "flushed between timed steps (512 MiB write)"},
+            "w_exec": checks / args.steps,
+            "w_exec_per_s": (checks / args.steps) / (ms_per_step * 1e-3),
+            "roofline": {"bound": "alu", "kernel": "k_screen (XOR+POPC+IMNMX)",
+                         "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tchecks/s",
+                         "frac": achieved / peak if peak else None, "traffic": load_traffic(),
+                         "peak_basis": f"{sms} SM x {POPC_PER_CLK_PER_SM} POPC/clk/SM x {sm_max:.0f} MHz "
+                                       "(POPC rate measured, profiles/r01_popc_peak.txt)",
+                         "screen_share_of_step": (screen_ms / args.steps) / ms_per_step,
+                         "screen_launches_per_step": stats[-1]["screen_launches"]},
+            "e2e": {"value": e2e_val, "unit": "checks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(sum(s["launches"] for s in stats)),
+            "clocks": clocks,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, desc = oracle_sample(n, d, o, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = {"value": v, "unit": "checks/s", "cores": 1, "kind": "oracle", "sample": desc}
+        print(json.dumps(line), flush=True)
+    comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="28,3,lex")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-log2", type=int, default=19, help="reference arm: ranks per step = 2^k")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

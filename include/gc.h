@@ -79,6 +79,8 @@ typedef struct gc_options {
 #define GC_FLAG_NO_EARLY_EXIT  0x1u  /* screen every candidate against the whole codebook, one phase     */
 #define GC_FLAG_SYNC_TILES     0x2u  /* host waits after every tile (debugging)                         */
 #define GC_FLAG_FORCE_SEQ_RESOLVE 0x4u /* in-tile resolve by the sequential fallback (testing)           */
+#define GC_FLAG_KERNEL_TIMING  0x8u  /* bracket every screen launch with CUDA events on the launching
+                                        stream; fills gc_stats.screen_ms (benchmarking)               */
 
 /* Counters of one construction (filled when a gc_stats* is passed). */
 typedef struct gc_stats {
@@ -95,6 +97,9 @@ typedef struct gc_stats {
     uint64_t resolve_checks; /* survivor-survivor distance evaluations in the in-tile resolve         */
     double w_def;            /* definitional work sum_j (2^n - 1 - rank_j): every candidate against
                                 every codeword accepted before it                       */
+    uint64_t launches;       /* kernels this call launched                                            */
+    uint64_t screen_launches;/* of which screen kernels (the dominant kernel)                         */
+    double screen_ms;        /* summed device time of the screen launches (GC_FLAG_KERNEL_TIMING)     */
 } gc_stats;
 
 /* ------------------------------------------------------------------ generate */
@@ -159,15 +164,23 @@ size_t gc_nccl_id_bytes(void);
  * (libnccl.so.2, loaded at run time) is unavailable. */
 int gc_nccl_unique_id(uint8_t *id, size_t id_bytes);
 
-/* One rank of a `world`-GPU construction (one process per GPU, current device = this
- * rank's GPU).  Every rank screens 1/world of each tile's candidates against its full
- * (replicated) codebook; the survivor bit-masks are all-gathered with NCCL once per tile;
- * every rank then resolves the tile identically, so all ranks end with the same code.
- * Buffers/stream/stats as gc_generate_device; the call synchronises `stream`.
- * world == 1 is allowed (no NCCL is used). */
+/* An NCCL communicator over `world` ranks (one process per GPU), created once and reused
+ * by every construction.  nccl_id: the bytes from gc_nccl_unique_id on one rank, shared
+ * with the others (e.g. broadcast over a torch.distributed process group); the current
+ * CUDA device must be this rank's GPU.  world must be a power of two in [1, 64];
+ * world == 1 needs no id (nccl_id may be NULL) and uses no NCCL.  GC_ENCCL on failure. */
+typedef struct gc_comm gc_comm;
+int gc_comm_create(const uint8_t *nccl_id, size_t id_bytes, int rank, int world, gc_comm **out_comm);
+int gc_comm_destroy(gc_comm *comm);   /* NULL is a no-op */
+
+/* One rank's part of a multi-GPU construction (comm == NULL: a single-GPU run).
+ * Every rank screens 1/world of each tile's candidates against its full (replicated)
+ * codebook; the per-tile survivor bit-masks are all-gathered with NCCL over NVLink once
+ * per tile; every rank then resolves the tile identically, so all ranks end with the
+ * same code in d_codebook.  Buffers/stream/stats as gc_generate_device; the call
+ * synchronises `stream`.  Every rank must call with identical (n, d, ordering, opt). */
 int gc_generate_rank(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt,
-                     int rank, int world, const uint8_t *nccl_id, size_t id_bytes,
-                     uint32_t *d_codebook, uint64_t capacity, uint64_t *d_count,
+                     gc_comm *comm, uint32_t *d_codebook, uint64_t capacity, uint64_t *d_count,
                      void *stream, gc_stats *stats);
 
 /* ------------------------------------------------------------------- misc */

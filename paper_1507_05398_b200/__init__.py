@@ -12,6 +12,7 @@ from __future__ import annotations
 
 from ._binding import (  # noqa: F401
     GC_FLAG_FORCE_SEQ_RESOLVE,
+    GC_FLAG_KERNEL_TIMING,
     GC_FLAG_NO_EARLY_EXIT,
     GC_FLAG_SYNC_TILES,
     GC_GRADED_LEX,
@@ -23,7 +24,10 @@ from ._binding import (  # noqa: F401
     LIB_PATH,
     exported_symbols,
     gc_abi_version,
+    GcComm,
     gc_capacity_bound,
+    gc_comm_create,
+    gc_comm_destroy,
     gc_generate,
     gc_generate_device,
     gc_generate_ex,
@@ -40,4 +44,4 @@ from ._binding import (  # noqa: F401
 )
 
 __all__ = [n for n in dir() if n.startswith("gc_") or n.startswith("GC_")] + [
-    "GCError", "ORDERINGS", "ordering_id", "LIB_PATH", "exported_symbols"]
+    "GCError", "GcComm", "ORDERINGS", "ordering_id", "LIB_PATH", "exported_symbols"]

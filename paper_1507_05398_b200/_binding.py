@@ -22,6 +22,7 @@ ORDERINGS = {"lex": GC_LEX, "gray": GC_GRAY, "glex": GC_GRADED_LEX, "grlex": GC_
 GC_FLAG_NO_EARLY_EXIT = 0x1
 GC_FLAG_SYNC_TILES = 0x2
 GC_FLAG_FORCE_SEQ_RESOLVE = 0x4
+GC_FLAG_KERNEL_TIMING = 0x8
 
 _STATUS = {0: "GC_OK", 1: "GC_EINVAL", 2: "GC_ERANGE", 3: "GC_ENOSPC", 4: "GC_EUNSUPPORTED",
            5: "GC_ECUDA", 6: "GC_ENOMEM", 7: "GC_ENCCL", 8: "GC_EINTERNAL"}
@@ -39,7 +40,8 @@ class gc_stats(ctypes.Structure):
                 ("M", ctypes.c_uint64), ("tiles", ctypes.c_uint64), ("phases", ctypes.c_uint64),
                 ("checks_exec", ctypes.c_uint64), ("survivors", ctypes.c_uint64),
                 ("conflicts", ctypes.c_uint64), ("resolve_checks", ctypes.c_uint64),
-                ("w_def", ctypes.c_double)]
+                ("w_def", ctypes.c_double), ("launches", ctypes.c_uint64),
+                ("screen_launches", ctypes.c_uint64), ("screen_ms", ctypes.c_double)]
 
     def to_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_ if name != "struct_size"}
@@ -71,10 +73,13 @@ _sig("gc_ranks_to_vectors_device", ctypes.c_int, [ctypes.c_int, ctypes.c_uint32,
                                                   ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p])
 _sig("gc_nccl_id_bytes", ctypes.c_size_t, [])
 _sig("gc_nccl_unique_id", ctypes.c_int, [_u8p, ctypes.c_size_t])
+_sig("gc_comm_create", ctypes.c_int, [_u8p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(ctypes.c_void_p)])
+_sig("gc_comm_destroy", ctypes.c_int, [ctypes.c_void_p])
 _sig("gc_generate_rank", ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int,
-                                        ctypes.POINTER(gc_options), ctypes.c_int, ctypes.c_int, _u8p,
-                                        ctypes.c_size_t, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p,
-                                        ctypes.c_void_p, ctypes.POINTER(gc_stats)])
+                                        ctypes.POINTER(gc_options), ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.POINTER(gc_stats)])
 _sig("gc_strerror", ctypes.c_char_p, [ctypes.c_int])
 _sig("gc_last_error", ctypes.c_char_p, [])
 _sig("gc_abi_version", ctypes.c_int, [])
@@ -216,19 +221,47 @@ def gc_nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def gc_generate_rank(n: int, d: int, ordering, rank: int, world: int, nccl_id: bytes | None,
-                     codebook, count, stream=None, options=None) -> dict:
-    """One rank of a multi-GPU construction (one process per GPU).  Returns the stats dict."""
-    o = _opts(options)
-    st = gc_stats()
-    st.struct_size = ctypes.sizeof(gc_stats)
+class GcComm:
+    """Owns a gc_comm* (gc_comm_create / gc_comm_destroy)."""
+
+    def __init__(self, handle: int, rank: int, world: int):
+        self.handle, self.rank, self.world = handle, rank, world
+
+    def close(self):
+        if self.handle:
+            _lib.gc_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gc_comm_create(nccl_id: bytes | None, rank: int, world: int) -> GcComm:
+    h = ctypes.c_void_p()
     if nccl_id is not None:
         idbuf = (ctypes.c_uint8 * len(nccl_id)).from_buffer_copy(nccl_id)
         idlen = len(nccl_id)
     else:
         idbuf, idlen = None, 0
+    _check(_lib.gc_comm_create(idbuf, idlen, rank, world, ctypes.byref(h)), "gc_comm_create")
+    return GcComm(h.value, rank, world)
+
+
+def gc_comm_destroy(comm: GcComm):
+    comm.close()
+
+
+def gc_generate_rank(n: int, d: int, ordering, comm: GcComm | None, codebook, count, stream=None,
+                     options=None) -> dict:
+    """One rank of a multi-GPU construction (one process per GPU).  Returns the stats dict."""
+    o = _opts(options)
+    st = gc_stats()
+    st.struct_size = ctypes.sizeof(gc_stats)
     cap = codebook.numel() * codebook.element_size() // 4
-    _check(_lib.gc_generate_rank(n, d, ordering_id(ordering), _ref(o), rank, world, idbuf, idlen,
+    _check(_lib.gc_generate_rank(n, d, ordering_id(ordering), _ref(o), comm.handle if comm else None,
                                  codebook.data_ptr(), cap, count.data_ptr(), _stream_ptr(stream),
                                  ctypes.byref(st)), "gc_generate_rank")
     return st.to_dict()

@@ -45,7 +45,8 @@ int resolve_options(const gc_options *opt, Options *out) {
         set_error("emulate_ranks must be a power of two in [1, 64]");
         return GC_EINVAL;
     }
-    if (o.flags & ~(uint32_t)(GC_FLAG_NO_EARLY_EXIT | GC_FLAG_SYNC_TILES | GC_FLAG_FORCE_SEQ_RESOLVE)) {
+    if (o.flags & ~(uint32_t)(GC_FLAG_NO_EARLY_EXIT | GC_FLAG_SYNC_TILES | GC_FLAG_FORCE_SEQ_RESOLVE |
+                              GC_FLAG_KERNEL_TIMING)) {
         set_error("unknown bits in gc_options.flags");
         return GC_EINVAL;
     }
@@ -310,36 +311,58 @@ int gc_nccl_unique_id(uint8_t *id, size_t id_bytes) {
     return GC_OK;
 }
 
-int gc_generate_rank(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt, int rank, int world,
-                     const uint8_t *nccl_id, size_t id_bytes, uint32_t *d_codebook, uint64_t capacity,
-                     uint64_t *d_count, void *stream, gc_stats *stats) {
+struct gc_comm {
+    int rank = 0, world = 1;
+    void *nccl = nullptr;
+};
+
+int gc_comm_create(const uint8_t *nccl_id, size_t id_bytes, int rank, int world, gc_comm **out_comm) {
+    clear_error();
+    if (!out_comm) { set_error("out_comm is NULL"); return GC_EINVAL; }
+    if (world < 1 || world > 64 || (world & (world - 1)) || rank < 0 || rank >= world) {
+        set_error("world must be a power of two in [1, 64] and 0 <= rank < world");
+        return GC_EINVAL;
+    }
+    if (world > 1 && (!nccl_id || id_bytes != sizeof(NcclUid))) { set_error("nccl_id must be 128 bytes"); return GC_EINVAL; }
+    gc_comm *c = new gc_comm;
+    c->rank = rank;
+    c->world = world;
+    if (world > 1) {
+        int rc = nccl_comm_init(&c->nccl, world, rank, nccl_id, id_bytes);
+        if (rc) { delete c; return rc; }
+    }
+    *out_comm = c;
+    return GC_OK;
+}
+
+int gc_comm_destroy(gc_comm *comm) {
+    if (!comm) return GC_OK;
+    nccl_comm_destroy(comm->nccl);
+    delete comm;
+    return GC_OK;
+}
+
+int gc_generate_rank(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt, gc_comm *comm,
+                     uint32_t *d_codebook, uint64_t capacity, uint64_t *d_count, void *stream, gc_stats *stats) {
     clear_error();
     int rc = validate_nd(n, d, ordering);
     if (rc) return rc;
     RunArgs a;
     rc = resolve_options(opt, &a.opt);
     if (rc) return rc;
-    if (world < 1 || world > 64 || (world & (world - 1)) || rank < 0 || rank >= world) {
-        set_error("world must be a power of two in [1, 64] and 0 <= rank < world");
+    if (comm && comm->world > 1 && a.opt.emulate_ranks != 1) { set_error("emulate_ranks needs a single rank"); return GC_EINVAL; }
+    if (!d_codebook || !d_count || capacity == 0) { set_error("d_codebook/d_count NULL or capacity 0"); return GC_EINVAL; }
+    if (stats && stats->struct_size != 0 && stats->struct_size < sizeof(gc_stats)) {
+        set_error("gc_stats.struct_size too small");
         return GC_EINVAL;
     }
-    if (a.opt.emulate_ranks != 1 && world != 1) { set_error("emulate_ranks needs world == 1"); return GC_EINVAL; }
-    if (!d_codebook || !d_count || capacity == 0) { set_error("d_codebook/d_count NULL or capacity 0"); return GC_EINVAL; }
-    if (world > 1 && (!nccl_id || id_bytes != 128)) { set_error("nccl_id must be 128 bytes"); return GC_EINVAL; }
     a.n = n; a.d = d; a.ordering = ordering;
     a.d_codebook = d_codebook; a.capacity = capacity; a.d_count = d_count;
-    a.stream = stream; a.rank = rank; a.world = world;
+    a.stream = stream;
+    if (comm) { a.rank = comm->rank; a.world = comm->world; a.nccl_comm = comm->nccl; }
     gc_stats local{};
     a.stats = stats ? stats : &local;   // the multi-process call always synchronises
-    void *comm = nullptr;
-    if (world > 1) {
-        rc = nccl_comm_init(&comm, world, rank, nccl_id, id_bytes);
-        if (rc) return rc;
-        a.nccl_comm = comm;
-    }
-    rc = engine_run(a);
-    if (comm) nccl_comm_destroy(comm);
-    return rc;
+    return engine_run(a);
 }
 
 }  // extern "C"

@@ -437,7 +437,18 @@ struct DeviceContext {
     unsigned long long *host_latest = nullptr;       // pinned, mapped
     unsigned long long *host_latest_dev = nullptr;   // its device alias
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> tev;   // GC_FLAG_KERNEL_TIMING event pool (pairs)
     std::mutex mu;
+
+    int timing_event(size_t i, cudaEvent_t *e) {
+        while (tev.size() <= i) {
+            cudaEvent_t x;
+            CK(cudaEventCreate(&x));
+            tev.push_back(x);
+        }
+        *e = tev[i];
+        return GC_OK;
+    }
 
     void release() {
         cudaFree(vals); cudaFree(dead); cudaFree(list[0]); cudaFree(list[1]);
@@ -527,7 +538,9 @@ int engine_run(const RunArgs &a) {
     const int edge_grid = cx->sm_count * 8;
     const unsigned long long cap_bound = a.capacity;
     std::vector<unsigned long long> tile_end;   // ranks covered after each tile
-    unsigned long long phases_total = 0;
+    unsigned long long phases_total = 0, launches = 0, screen_launches = 0;
+    const bool timing = (o.flags & GC_FLAG_KERNEL_TIMING) != 0;
+    size_t nev = 0;
 
     CK(cudaEventRecord(cx->ev0, st));
     unsigned long long t0 = 0, tile = 0;
@@ -564,14 +577,23 @@ int engine_run(const RunArgs &a) {
             const uint2 *lin = nullptr;
             const unsigned int *cin = nullptr;
             for (int p = 0; p < P; ++p) {
+                cudaEvent_t ea = nullptr, eb = nullptr;
+                if (timing) {
+                    if ((rc = cx->timing_event(nev++, &ea)) || (rc = cx->timing_event(nev++, &eb))) return rc;
+                    CK(cudaEventRecord(ea, st));
+                }
                 k_screen<<<screen_grid, kScreenThreads, 0, st>>>(p, P, o.window0, early, a.d_codebook, cx->vals,
                                                                 lin, cin, plo, part, cx->dead, cx->ctr, a.d);
+                if (timing) CK(cudaEventRecord(eb, st));
+                ++launches;
+                ++screen_launches;
                 if (p + 1 < P) {
                     uint2 *lout = cx->list[p & 1];
                     unsigned int *cout = &cx->ctr->list_count[g * kMaxPhases + p];
                     const uint32_t L_ub = part;
                     k_compact<<<std::min<uint32_t>((L_ub + 255) / 256, (uint32_t)cx->sm_count * 4), 256, 0, st>>>(
                         cx->vals, lin, cin, plo, part, cx->dead, lout, cout);
+                    ++launches;
                     lin = lout;
                     cin = cout;
                 }
@@ -589,6 +611,7 @@ int engine_run(const RunArgs &a) {
         k_commit<<<1, kResolveThreads, 0, st>>>(cx->surv, cx->edges, cx->status, cx->blocked, a.d_codebook,
                                                 a.capacity, a.d, t0, N - 1, force_seq, cx->ctr, tile,
                                                 cx->host_latest_dev);
+        launches += 4;   // gen, gather, edges, commit
         CK(cudaGetLastError());
         t0 += K;
         tile_end.push_back(t0);
@@ -596,6 +619,7 @@ int engine_run(const RunArgs &a) {
         if (o.flags & GC_FLAG_SYNC_TILES) CK(cudaStreamSynchronize(st));
     }
     k_finish<<<1, 1, 0, st>>>(cx->ctr, (unsigned long long *)a.d_count);
+    ++launches;
     CK(cudaEventRecord(cx->ev1, st));
     CK(cudaGetLastError());
 
@@ -617,6 +641,14 @@ int engine_run(const RunArgs &a) {
         s->conflicts = h.conflicts;
         s->resolve_checks = h.resolve_checks;
         s->w_def = (double)h.w_def;
+        s->launches = launches;
+        s->screen_launches = screen_launches;
+        s->screen_ms = 0;
+        for (size_t i = 0; i + 1 < nev; i += 2) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, cx->tev[i], cx->tev[i + 1]));
+            s->screen_ms += t;
+        }
         s->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }

@@ -72,10 +72,18 @@ def test_device_entry_points_validate():
     assert B._lib.gc_ranks_to_vectors_device(0, 8, 250, 10, 1, None) == 2         # out of range
     assert B._lib.gc_ranks_to_vectors_device(0, 33, 0, 1, 1, None) == 4
     assert B._lib.gc_ranks_to_vectors_device(7, 8, 0, 1, 1, None) == 1
-    # rank entry: bad world / rank / id
-    assert B._lib.gc_generate_rank(7, 3, 0, None, 0, 3, None, 0, 1, 16, 1, None, None) == 1
-    assert B._lib.gc_generate_rank(7, 3, 0, None, 2, 2, None, 0, 1, 16, 1, None, None) == 1
-    assert B._lib.gc_generate_rank(7, 3, 0, None, 0, 2, None, 0, 1, 16, 1, None, None) == 1
+    # communicator: bad world / rank / id
+    h = ctypes.c_void_p()
+    assert B._lib.gc_comm_create(None, 0, 0, 3, ctypes.byref(h)) == 1
+    assert B._lib.gc_comm_create(None, 0, 2, 2, ctypes.byref(h)) == 1
+    assert B._lib.gc_comm_create(None, 0, 0, 2, ctypes.byref(h)) == 1
+    assert B._lib.gc_comm_create(None, 0, 0, 1, None) == 1
+    c = gc.gc_comm_create(None, 0, 1)          # world 1: no NCCL needed
+    assert c.handle
+    assert B._lib.gc_generate_rank(7, 8, 0, None, c.handle, 1, 16, 1, None, None) == 1
+    assert B._lib.gc_generate_rank(7, 3, 0, None, c.handle, None, 16, 1, None, None) == 1
+    gc.gc_comm_destroy(c)
+    assert B._lib.gc_comm_destroy(None) == 0
 
 
 def test_capacity_bound():

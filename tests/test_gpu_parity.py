@@ -220,7 +220,9 @@ def test_rank_entry_world1(gc):
     cap = gc.gc_capacity_bound(n, d)
     cb = torch.empty(cap, dtype=torch.int32, device="cuda")
     cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
-    st = gc.gc_generate_rank(n, d, o, 0, 1, None, cb, cnt)
+    comm = gc.gc_comm_create(None, 0, 1)
+    st = gc.gc_generate_rank(n, d, o, comm, cb, cnt)
+    comm.close()
     M = int(cnt.item())
     assert st["M"] == M
     assert np.array_equal(cb[:M].cpu().numpy().view(np.uint32), O.greedy_ball(n, d, o))
