@@ -16,7 +16,10 @@ $(SRC)/gc_engine.o: $(SRC)/gc_engine.cu $(SRC)/gc_order.cuh $(SRC)/gc_internal.h
 $(SRC)/gc_abi.o: $(SRC)/gc_abi.cpp $(SRC)/gc_internal.h include/gc.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC,-Wall -x cu -c $< -o $@
 
-$(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o
+$(SRC)/gc_persistent.o: $(SRC)/gc_persistent.cu $(SRC)/gc_order.cuh $(SRC)/gc_internal.h include/gc.h
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_persistent.ptxas.log || (cat $(SRC)/gc_persistent.ptxas.log; false)
+
+$(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o $(SRC)/gc_persistent.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
 $(ORACLE): oracle/greedy_oracle.c

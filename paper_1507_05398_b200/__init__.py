@@ -13,6 +13,7 @@ from __future__ import annotations
 from ._binding import (  # noqa: F401
     GC_FLAG_FORCE_SEQ_RESOLVE,
     GC_FLAG_KERNEL_TIMING,
+    GC_FLAG_LAUNCHED_TILES,
     GC_FLAG_NO_EARLY_EXIT,
     GC_FLAG_SYNC_TILES,
     GC_GRADED_LEX,

@@ -32,8 +32,8 @@ int resolve_options(const gc_options *opt, Options *out) {
         if (opt->emulate_ranks) o.emulate_ranks = opt->emulate_ranks;
         o.flags = opt->flags;
     }
-    if (!is_pow2(o.tile_min) || o.tile_min < 32 || !is_pow2(o.tile_max) || o.tile_max > (1u << 20) ||
-        o.tile_min > o.tile_max) {
+    if (!is_pow2(o.tile_min) || o.tile_min < 32 || (o.tile_max && (!is_pow2(o.tile_max) || o.tile_max > (1u << 20) ||
+        o.tile_min > o.tile_max))) {
         set_error("tile_min/tile_max must be powers of two with 32 <= tile_min <= tile_max <= 2^20");
         return GC_EINVAL;
     }
@@ -46,7 +46,7 @@ int resolve_options(const gc_options *opt, Options *out) {
         return GC_EINVAL;
     }
     if (o.flags & ~(uint32_t)(GC_FLAG_NO_EARLY_EXIT | GC_FLAG_SYNC_TILES | GC_FLAG_FORCE_SEQ_RESOLVE |
-                              GC_FLAG_KERNEL_TIMING)) {
+                              GC_FLAG_KERNEL_TIMING | GC_FLAG_LAUNCHED_TILES)) {
         set_error("unknown bits in gc_options.flags");
         return GC_EINVAL;
     }

@@ -30,6 +30,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <map>
 #include <memory>
@@ -66,6 +68,8 @@ struct DevCounters {
     unsigned int edge_overflow;
     unsigned int error;                 // 1 = capacity exceeded
     unsigned int list_count[kMaxParts * kMaxPhases];
+    unsigned long long phase_checks[kMaxPhases];   // diagnostics (GC_DEBUG_PHASES)
+    unsigned long long phase_alive[kMaxPhases];
 };
 
 #define CK(call)                                                                              \
@@ -127,6 +131,7 @@ k_screen(int p, int P, uint32_t W0, bool early_exit, const uint32_t *__restrict_
     if (hi <= lo) return;
     const uint32_t L = list ? *list_count : part_n;
     if (L == 0) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ctr->phase_alive[p], (unsigned long long)L);
     const uint32_t wlen = (uint32_t)(hi - lo);
     const uint32_t nchunks = (wlen + kChunk - 1) / kChunk;
     const uint32_t ncb = (L + kScreenCB - 1) / kScreenCB;
@@ -197,7 +202,10 @@ k_screen(int p, int P, uint32_t W0, bool early_exit, const uint32_t *__restrict_
         }
         __syncthreads();   // before the next item overwrites cw
     }
-    if (lane == 0 && my_checks) atomicAdd(&ctr->checks_exec, my_checks);
+    if (lane == 0 && my_checks) {
+        atomicAdd(&ctr->checks_exec, my_checks);
+        atomicAdd(&ctr->phase_checks[p], my_checks);
+    }
 }
 
 // survivors of a window -> dense list for the next window (order irrelevant here)
@@ -511,12 +519,20 @@ static int phases_for(unsigned long long M_ub, uint32_t W0) {
 
 int engine_run(const RunArgs &a) {
     auto wall0 = std::chrono::steady_clock::now();
+    if (persistent_supported(a)) {
+        int rc = persistent_run(a);
+        if (a.stats) a.stats->wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+        return rc;
+    }
     int device;
     CK(cudaGetDevice(&device));
     DeviceContext *cx = context_for(device);
     std::lock_guard<std::mutex> lock(cx->mu);
     cudaStream_t st = (cudaStream_t)a.stream;
-    const Options &o = a.opt;
+    Options o = a.opt;
+    if (!o.tile_max) o.tile_max = 65536;
+    if (o.tile_min > o.tile_max) o.tile_min = o.tile_max;
     const unsigned parts_local = (a.world > 1) ? 1u : o.emulate_ranks;   // partitions screened here
     const unsigned G = (a.world > 1) ? (unsigned)a.world : o.emulate_ranks; // partitions per tile
     const uint32_t Kpad_max = std::max<uint32_t>(o.tile_max, 32u * G);
@@ -650,6 +666,13 @@ int engine_run(const RunArgs &a) {
             s->screen_ms += t;
         }
         s->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+        if (getenv("GC_DEBUG_PHASES")) {
+            for (int p = 0; p < kMaxPhases; ++p)
+                if (h.phase_alive[p])
+                    fprintf(stderr, "[gc] phase %2d: alive %.4g  checks %.4g  (%.1f%% of screen)\n", p,
+                            (double)h.phase_alive[p], (double)h.phase_checks[p],
+                            100.0 * (double)h.phase_checks[p] / (double)(h.checks_exec ? h.checks_exec : 1));
+        }
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }
     return GC_OK;

@@ -17,7 +17,7 @@ void clear_error();
 // resolved schedule options (defaults applied, validated)
 struct Options {
     uint32_t tile_min = 256;
-    uint32_t tile_max = 65536;
+    uint32_t tile_max = 0;          // 0 = engine default (persistent 4096, launched 65536)
     uint32_t window0 = 1024;
     uint32_t emulate_ranks = 1;
     uint32_t flags = 0;
@@ -55,6 +55,8 @@ struct RunArgs {
     gc_stats *stats = nullptr;      // non-null -> synchronise and fill
 };
 int engine_run(const RunArgs &a);
+bool persistent_supported(const RunArgs &a);   // gc_persistent.cu
+int persistent_run(const RunArgs &a);
 int engine_ranks_to_vectors_device(int ordering, uint32_t n, uint64_t first, uint64_t count,
                                    uint32_t *d_out, void *stream);
 

@@ -173,11 +173,17 @@ SCHEDULES = [
     {"emulate_ranks": 2},
     {"emulate_ranks": 8, "tile_min": 256},
     {"emulate_ranks": 4, "flags": 1},
+    {"flags": 16},                      # host-launched tiles (default 65536)
+    {"flags": 16, "tile_max": 4096, "window0": 256},
+    {"tile_max": 8192},                 # persistent kernel, largest tile
+    {"tile_min": 32, "tile_max": 256, "window0": 64},
+    {"tile_min": 1024, "tile_max": 1024, "window0": 1 << 14},
 ]
 
 
 @pytest.mark.parametrize("sched", SCHEDULES, ids=lambda s: "-".join(f"{k}{v}" for k, v in s.items()))
-@pytest.mark.parametrize("n,d,o", [(16, 3, "lex"), (17, 5, "glex"), (18, 4, "grlex"), (15, 6, "gray")])
+@pytest.mark.parametrize("n,d,o", [(16, 3, "lex"), (17, 5, "glex"), (18, 4, "grlex"), (15, 6, "gray"),
+                                   (20, 3, "gray")])
 def test_schedule_invariance(gc, sched, n, d, o):
     w, st = gpu_code(gc, n, d, o, **sched)
     assert np.array_equal(w, O.greedy_ball(n, d, o)), sched
