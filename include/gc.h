@@ -75,6 +75,8 @@ typedef struct gc_options {
     uint32_t emulate_ranks;  /* >1: split every tile's candidates into this many partitions on ONE GPU,
                                 exactly as gc_generate_rank splits them across GPUs (testing), default 1 */
     uint32_t flags;          /* GC_FLAG_* below                                                          */
+    uint32_t window_growth;  /* log2 of the factor by which each newest-first window grows over the
+                                previous one (1 = doubling ... 4 = x16), default 2                         */
 } gc_options;
 
 #define GC_FLAG_NO_EARLY_EXIT  0x1u  /* screen every candidate against the whole codebook, one phase     */

@@ -32,7 +32,8 @@ _STATUS = {0: "GC_OK", 1: "GC_EINVAL", 2: "GC_ERANGE", 3: "GC_ENOSPC", 4: "GC_EU
 class gc_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("tile_min", ctypes.c_uint32),
                 ("tile_max", ctypes.c_uint32), ("window0", ctypes.c_uint32),
-                ("emulate_ranks", ctypes.c_uint32), ("flags", ctypes.c_uint32)]
+                ("emulate_ranks", ctypes.c_uint32), ("flags", ctypes.c_uint32),
+                ("window_growth", ctypes.c_uint32)]
 
 
 class gc_stats(ctypes.Structure):

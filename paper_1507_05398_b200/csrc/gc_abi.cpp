@@ -31,6 +31,11 @@ int resolve_options(const gc_options *opt, Options *out) {
         if (opt->window0) o.window0 = opt->window0;
         if (opt->emulate_ranks) o.emulate_ranks = opt->emulate_ranks;
         o.flags = opt->flags;
+        if (opt->window_growth) o.growth = opt->window_growth;
+    }
+    if (o.growth < 1 || o.growth > 4) {
+        set_error("window_growth must be in [1, 4]");
+        return GC_EINVAL;
     }
     if (!is_pow2(o.tile_min) || o.tile_min < 32 || (o.tile_max && (!is_pow2(o.tile_max) || o.tile_max > (1u << 20) ||
         o.tile_min > o.tile_max))) {

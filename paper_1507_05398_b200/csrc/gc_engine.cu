@@ -114,7 +114,7 @@ __global__ void k_gen_tile(const OrderTables *__restrict__ tab, int ord, int n, 
 //   window: newest-first positions [b_p, b_{p+1}) with b_p = W0 (2^p - 1); last phase to 0.
 // Work item = (block of kScreenCB candidates) x (chunk of kChunk codewords).
 __global__ void __launch_bounds__(kScreenThreads)
-k_screen(int p, int P, uint32_t W0, bool early_exit, const uint32_t *__restrict__ codebook,
+k_screen(int p, int P, uint32_t W0, int growth, bool early_exit, const uint32_t *__restrict__ codebook,
          const uint32_t *__restrict__ vals, const uint2 *__restrict__ list, const unsigned int *list_count,
          uint32_t part_lo, uint32_t part_n, uint32_t *dead, DevCounters *ctr, uint32_t d) {
     __shared__ __align__(16) uint32_t cw[kChunk];
@@ -123,7 +123,9 @@ k_screen(int p, int P, uint32_t W0, bool early_exit, const uint32_t *__restrict_
     if (!early_exit) {
         hi = M; lo = 0;
     } else {
-        const long long bp = (long long)W0 * ((1ll << p) - 1), bq = (long long)W0 * ((1ll << (p + 1)) - 1);
+        long long bp = 0, w = W0;
+        for (int i = 0; i < p; ++i) { bp += w; w <<= growth; }
+        const long long bq = bp + w;
         hi = M - bp;
         lo = (p == P - 1) ? 0 : M - bq;
         if (lo < 0) lo = 0;
@@ -508,10 +510,11 @@ static uint32_t tile_size(const Options &o, unsigned long long t0) {
     return K;
 }
 
-static int phases_for(unsigned long long M_ub, uint32_t W0) {
+static int phases_for(unsigned long long M_ub, uint32_t W0, uint32_t growth) {
     if (M_ub == 0) return 0;
     int P = 1;
-    while (P < kMaxPhases && (unsigned long long)W0 * ((1ull << P) - 1) < M_ub) ++P;
+    unsigned long long depth = W0, w = W0;
+    while (P < kMaxPhases && depth < M_ub) { w <<= growth; depth += w; ++P; }
     return P;
 }
 
@@ -581,7 +584,7 @@ int engine_run(const RunArgs &a) {
                 M_ub = std::min(M_ub, Mk + (t0 - tile_end[k]));
             }
         }
-        int P = early ? phases_for(M_ub, o.window0) : 1;
+        int P = early ? phases_for(M_ub, o.window0, o.growth) : 1;
         if (t0 == 0) P = 0;            // empty codebook before the first tile
         else if (P < 1) P = 1;
 
@@ -598,7 +601,7 @@ int engine_run(const RunArgs &a) {
                     if ((rc = cx->timing_event(nev++, &ea)) || (rc = cx->timing_event(nev++, &eb))) return rc;
                     CK(cudaEventRecord(ea, st));
                 }
-                k_screen<<<screen_grid, kScreenThreads, 0, st>>>(p, P, o.window0, early, a.d_codebook, cx->vals,
+                k_screen<<<screen_grid, kScreenThreads, 0, st>>>(p, P, o.window0, (int)o.growth, early, a.d_codebook, cx->vals,
                                                                 lin, cin, plo, part, cx->dead, cx->ctr, a.d);
                 if (timing) CK(cudaEventRecord(eb, st));
                 ++launches;

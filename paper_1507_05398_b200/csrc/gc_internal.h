@@ -21,6 +21,7 @@ struct Options {
     uint32_t window0 = 1024;
     uint32_t emulate_ranks = 1;
     uint32_t flags = 0;
+    uint32_t growth = 2;            // log2 window growth per level
 };
 int resolve_options(const gc_options *opt, Options *out);   // GC_OK / GC_EINVAL
 

@@ -37,11 +37,14 @@ constexpr int kPThreads = 512;              // threads per CTA (16 warps); grid 
 constexpr int kPWarps = kPThreads / 32;
 constexpr int kPR = 2;                      // candidates per lane
 constexpr int kPBatch = 32 * kPR;           // candidates per warp item
-constexpr uint32_t kPSub = 512;             // codewords per warp item
+constexpr uint32_t kPSubMin = 64;           // codewords per warp item: at least ...
+constexpr uint32_t kPSubMax = 2048;         // ... and at most
 constexpr int kPMaxLevels = 32;
 constexpr uint32_t kPMaxTile = 1u << 13;    // largest tile for this engine (survivors fit in smem)
 constexpr uint32_t kPMaxBatches = kPMaxTile / kPBatch;
-constexpr size_t kPDynSmem = kPMaxTile * 7;     // s_val (4 B) + s_idx (2 B) + s_status (1 B)
+constexpr int kPAdj = 8;                        // earlier in-tile conflicts recorded per survivor
+// resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + s_adjn (1 B) + s_adj (2 B x kPAdj)
+constexpr size_t kPDynSmem = (size_t)kPMaxTile * (8 + 2 * kPAdj);
 
 struct PState {
     unsigned long long M;
@@ -52,6 +55,10 @@ struct PState {
     unsigned long long w_def;
     unsigned long long tiles;
     unsigned long long levels;
+    unsigned long long t_level[kPMaxLevels];   // diagnostics: CTA 0's view, ns (%globaltimer)
+    unsigned long long t_resolve, t_sync, t_tile;
+    unsigned long long t_r[6];                 // resolve sub-steps
+    unsigned long long n_overflow, n_seq, n_rounds;
     unsigned int error;
     unsigned int q_count[kPMaxLevels + 1];
     unsigned int bfin[kPMaxLevels][kPMaxBatches];
@@ -62,6 +69,7 @@ struct PArgs {
     uint32_t d;
     unsigned long long N;           // 2^n
     uint32_t tile_min, tile_max, W0;
+    int growth;
     uint32_t *codebook;
     unsigned long long capacity;
     const OrderTables *tabs;
@@ -72,6 +80,7 @@ struct PArgs {
     uint8_t *status;                // [kPMaxTile]
     PState *st;
     unsigned long long *d_count;
+    int timing;
 };
 
 __device__ __forceinline__ uint32_t p_tile_size(const PArgs &a, unsigned long long t0) {
@@ -81,57 +90,58 @@ __device__ __forceinline__ uint32_t p_tile_size(const PArgs &a, unsigned long lo
     return K;
 }
 
-// number of levels needed to reach codeword 0 from the newest, windows W0 * 2^l
-__device__ __forceinline__ int p_levels(unsigned long long M, uint32_t W0) {
+// newest-first depth covered by levels 0 .. l-1: W0 (1 + g + ... + g^(l-1)), g = 2^growth
+__device__ __forceinline__ unsigned long long p_depth(uint32_t W0, int growth, int l) {
+    unsigned long long dsum = 0, w = W0;
+    for (int i = 0; i < l; ++i) { dsum += w; w <<= growth; }
+    return dsum;
+}
+
+// number of levels needed to reach codeword 0 from the newest
+__device__ __forceinline__ int p_levels(unsigned long long M, uint32_t W0, int growth) {
     if (M == 0) return 0;
     int L = 1;
-    while (L < kPMaxLevels && (unsigned long long)W0 * ((1ull << L) - 1) < M) ++L;
+    while (L < kPMaxLevels && p_depth(W0, growth, L) < M) ++L;
     return L;
 }
 
 // scan codewords [a, b) newest first for the lane's kPR candidates; returns the number of
-// codewords scanned (for the work counter).  Early exit when every lane's candidates are dead.
+// codewords scanned (for the work counter).  The warp reads 32 codewords per coalesced
+// 128-byte load (lane k holds codeword top-1-k), prefetches the next block while it works
+// on this one, and broadcasts each codeword with a shuffle.  Early exit (warp vote) after
+// every block once every lane's candidates are dead.
 __device__ __forceinline__ uint32_t p_scan(const uint32_t *__restrict__ cb, long long a, long long b,
-                                           const uint32_t (&v)[kPR], uint32_t (&m)[kPR], uint32_t d) {
-    long long hi = b;
+                                           uint32_t cur, const uint32_t (&v)[kPR], uint32_t (&m)[kPR],
+                                           uint32_t d) {
+    const int lane = threadIdx.x & 31;
+    long long top = b;
     uint32_t scanned = 0;
-    // unaligned top part (scalar) so that the body is 16-byte aligned
-    while (hi > a && (hi & 3)) {
-        const uint32_t c = __ldcg(cb + hi - 1);
+    while (top > a) {
+        const long long ntop = top - 32;
+        const uint32_t nxt = (ntop > a && ntop - 1 - lane >= a) ? __ldcg(cb + ntop - 1 - lane) : 0u;
+        const long long nv = top - a;
+        if (nv >= 32) {
 #pragma unroll
-        for (int r = 0; r < kPR; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
-        --hi;
-        ++scanned;
-    }
-    const uint4 *cb4 = reinterpret_cast<const uint4 *>(cb);
-    long long g = hi >> 2;                    // groups [a4, g)
-    const long long a4 = (a + 3) >> 2;
-    int it = 0;
-    while (g > a4) {
-        if ((it++ & 7) == 0) {
-            bool done = true;
+            for (int k = 0; k < 32; ++k) {
+                const uint32_t c = __shfl_sync(0xffffffffu, cur, k);
 #pragma unroll
-            for (int r = 0; r < kPR; ++r) done &= (m[r] < d);
-            if (__all_sync(0xffffffffu, done)) return scanned;
+                for (int r = 0; r < kPR; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
+            }
+            scanned += 32;
+        } else {
+            for (int k = 0; k < (int)nv; ++k) {
+                const uint32_t c = __shfl_sync(0xffffffffu, cur, k);
+#pragma unroll
+                for (int r = 0; r < kPR; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
+            }
+            scanned += (uint32_t)nv;
         }
-        const uint4 c = __ldcg(cb4 + g - 1);
+        bool done = true;
 #pragma unroll
-        for (int r = 0; r < kPR; ++r) {
-            m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c.w));
-            m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c.z));
-            m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c.y));
-            m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c.x));
-        }
-        --g;
-        scanned += 4;
-    }
-    hi = g << 2;
-    while (hi > a) {                          // unaligned bottom part
-        const uint32_t c = __ldcg(cb + hi - 1);
-#pragma unroll
-        for (int r = 0; r < kPR; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
-        --hi;
-        ++scanned;
+        for (int r = 0; r < kPR; ++r) done &= (m[r] < d);
+        if (__all_sync(0xffffffffu, done)) break;
+        cur = nxt;
+        top = ntop;
     }
     return scanned;
 }
@@ -164,6 +174,12 @@ __device__ __forceinline__ uint32_t p_block_scan(uint32_t x, uint32_t *total, ui
     return r;
 }
 
+__device__ __forceinline__ unsigned long long p_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t C[33][33];
@@ -173,6 +189,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
     uint32_t *s_val = reinterpret_cast<uint32_t *>(p_dyn);
     uint16_t *s_idx = reinterpret_cast<uint16_t *>(p_dyn + kPMaxTile * 4);
     uint8_t *s_status = p_dyn + kPMaxTile * 6;
+    uint8_t *s_adjn = p_dyn + kPMaxTile * 7;
+    uint16_t *s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPMaxTile * 8);
     PState *st = a.st;
     const bool graded = a.ord >= GRADED_LEX;
     if (graded) {
@@ -189,26 +207,41 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
     while (t0 < a.N) {
         const uint32_t K = p_tile_size(a, t0);
         const unsigned long long M = __ldcg(&st->M);
-        const int L = p_levels(M, a.W0);
+        const int L = p_levels(M, a.W0, a.growth);
         const uint32_t W0 = a.W0;
+        const bool timer = a.timing && blockIdx.x == 0 && threadIdx.x == 0;
+        unsigned long long tm = timer ? p_now() : 0, tm_tile = tm;
 
         for (int l = 0; l < L; ++l) {
             // window of level l (newest-first positions), last level reaches 0
-            const long long bp = (long long)W0 * ((1ll << l) - 1);
+            const long long bp = (long long)p_depth(W0, a.growth, l);
             const long long hi = (long long)M - bp;
-            long long lo = (l == L - 1) ? 0 : hi - ((long long)W0 << l);
+            long long lo = (l == L - 1) ? 0 : hi - ((long long)W0 << (a.growth * l));
             if (lo < 0) lo = 0;
             const uint32_t n_l = (l == 0) ? K : __ldcg(&st->q_count[l]);
             const uint2 *qin = (l == 0) ? nullptr : ((l & 1) ? a.q1 : a.q0);
             uint2 *qout = (l & 1) ? a.q0 : a.q1;
             const uint32_t B = (n_l + kPBatch - 1) / kPBatch;
-            // sub-ranges aligned to absolute multiples of kPSub
-            const long long c_top = (hi + kPSub - 1) / kPSub, c_bot = lo / kPSub;
-            const uint32_t nsub = (hi > lo) ? (uint32_t)(c_top - c_bot) : 0u;
+            // sub-ranges of the window, newest first, sized so the level has ~4 items per warp
+            const long long wlen = hi - lo;
+            long long sub = 0;
+            uint32_t nsub = 0;
+            if (wlen > 0 && B > 0) {
+                const long long want = ((long long)nwarps * 4 + B - 1) / B;     // sub-ranges wanted
+                sub = (wlen + want - 1) / want;
+                sub = (sub + 31) & ~31ll;
+                sub = max(sub, (long long)kPSubMin);
+                sub = min(sub, (long long)kPSubMax);
+                nsub = (uint32_t)((wlen + sub - 1) / sub);
+            }
             const unsigned long long items = (unsigned long long)B * nsub;
             for (unsigned long long it = gwarp; it < items; it += nwarps) {
                 const uint32_t j = (uint32_t)(it / B), b = (uint32_t)(it % B);
-                // candidates of batch b
+                const long long s_hi = hi - (long long)j * sub;            // j = 0: newest
+                const long long s_lo = max(lo, s_hi - sub);
+                // first codeword block in flight while the candidates are fetched
+                const uint32_t cur0 = (s_hi - 1 - lane >= s_lo) ? __ldcg(a.codebook + s_hi - 1 - lane) : 0u;
+                // candidates of batch b (level 0: generated from their ranks)
                 uint32_t v[kPR], m[kPR], idx[kPR];
                 bool live[kPR];
 #pragma unroll
@@ -222,59 +255,61 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                             idx[r] = pos;
                             v[r] = rank_to_vector32(a.ord, a.n, C, off, t0 + pos);
                             if (j == 0) a.vals[pos] = v[r];
+                            // other sub-ranges of this level may already have killed it
+                            if (nsub > 1) live[r] = !((__ldcg(a.dead + (pos >> 5)) >> (pos & 31)) & 1u);
                         }
-                        live[r] = !((__ldcg(a.dead + (idx[r] >> 5)) >> (idx[r] & 31)) & 1u);
                     }
                     m[r] = live[r] ? 64u : 0u;
                 }
-                const long long cidx = c_top - 1 - (long long)j;          // j = 0: newest chunk
-                const long long s_lo = max(lo, cidx * (long long)kPSub);
-                const long long s_hi = min(hi, (cidx + 1) * (long long)kPSub);
                 bool any = false;
 #pragma unroll
                 for (int r = 0; r < kPR; ++r) any |= live[r];
+                bool kill[kPR];
+#pragma unroll
+                for (int r = 0; r < kPR; ++r) kill[r] = false;
                 if (__any_sync(0xffffffffu, any)) {
-                    const uint32_t sc = p_scan(a.codebook, s_lo, s_hi, v, m, a.d);
+                    const uint32_t sc = p_scan(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
                     my_checks += (unsigned long long)sc * kPR;   // per lane; summed over lanes below
 #pragma unroll
                     for (int r = 0; r < kPR; ++r) {
-                        const bool kill = live[r] && m[r] < a.d;
+                        kill[r] = live[r] && m[r] < a.d;
                         if (!qin) {
-                            const unsigned bb = __ballot_sync(0xffffffffu, kill);
+                            const unsigned bb = __ballot_sync(0xffffffffu, kill[r]);
                             if (lane == 0 && bb) atomicOr(&a.dead[idx[r] >> 5], bb);
-                        } else if (kill) {
+                        } else if (kill[r]) {
                             atomicOr(&a.dead[idx[r] >> 5], 1u << (idx[r] & 31));
                         }
                     }
                 }
                 if (l + 1 < L) {
                     // the warp finishing batch b's last item pushes its live candidates
-                    __threadfence();
-                    unsigned last = 0;
-                    if (lane == 0) last = (atomicAdd(&st->bfin[l][b], 1u) + 1u == nsub);
-                    last = __shfl_sync(0xffffffffu, last, 0);
-                    if (last) {
+                    unsigned last = 1;
+                    if (nsub > 1) {
                         __threadfence();
+                        if (lane == 0) last = (atomicAdd(&st->bfin[l][b], 1u) + 1u == nsub);
+                        last = __shfl_sync(0xffffffffu, last, 0);
+                        if (last) __threadfence();
+                    }
+                    if (last) {
 #pragma unroll
                         for (int r = 0; r < kPR; ++r) {
                             const uint32_t pos = b * kPBatch + r * 32 + lane;
                             bool alive = pos < n_l;
-                            uint2 e = make_uint2(0, 0);
                             if (alive) {
-                                if (qin) e = __ldcg(qin + pos);
-                                else { e.x = pos; e.y = v[r]; }
-                                alive = !((__ldcg(a.dead + (e.x >> 5)) >> (e.x & 31)) & 1u);
+                                if (nsub > 1) alive = !((__ldcg(a.dead + (idx[r] >> 5)) >> (idx[r] & 31)) & 1u);
+                                else alive = !kill[r];
                             }
                             const unsigned bb = __ballot_sync(0xffffffffu, alive);
                             unsigned base = 0;
                             if (lane == 0 && bb) base = atomicAdd(&st->q_count[l + 1], (unsigned)__popc(bb));
                             base = __shfl_sync(0xffffffffu, base, 0);
-                            if (alive) qout[base + __popc(bb & ((1u << lane) - 1u))] = e;
+                            if (alive) qout[base + __popc(bb & ((1u << lane) - 1u))] = make_uint2(idx[r], v[r]);
                         }
                     }
                 }
             }
             grid.sync();
+            if (timer) { const unsigned long long t = p_now(); st->t_level[l] += t - tm; tm = t; }
         }
 
         // ------------------------------------------------ resolve + commit (CTA 0)
@@ -307,32 +342,87 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                 S += tot;
             }
             __syncthreads();
-            // status: 1 = accepted (no earlier in-tile conflict), 2 = undecided (has one)
+            unsigned long long tr = timer ? p_now() : 0;
+#define P_TR(i) if (timer) { const unsigned long long t_ = p_now(); st->t_r[i] += t_ - tr; tr = t_; }
+            if (timer) st->t_r[0] += tr - tm;
+            // in-tile conflicts: s_adj[j] lists (up to kPAdj) earlier survivors within distance
+            // < d of survivor j (s_adjn = 255: more than kPAdj).  status 1 = accepted,
+            // 0 = rejected, 2 = undecided.
+            __shared__ unsigned long long s_stat[3];
+            if (tid < 3) s_stat[tid] = 0;
+            __syncthreads();
             unsigned long long rchk = 0, confl = 0;
             for (uint32_t j = tid; j < S; j += blockDim.x) {
                 const uint32_t vj = s_val[j];
-                uint32_t has = 0;
-                for (uint32_t k = 0; k < j; ++k) has |= (uint32_t)__popc(vj ^ s_val[k]) < a.d;
+                uint32_t cnt = 0;
+                for (uint32_t k = 0; k < j; ++k) {
+                    if ((uint32_t)__popc(vj ^ s_val[k]) < a.d) {
+                        if (cnt < kPAdj) s_adj[j * kPAdj + cnt] = (uint16_t)k;
+                        ++cnt;
+                    }
+                }
                 rchk += j;
-                s_status[j] = has ? 2 : 1;
-                confl += has;
+                s_adjn[j] = cnt > kPAdj ? 255 : (uint8_t)cnt;
+                if (a.timing && cnt > kPAdj) atomicAdd(&st->n_overflow, 1ull);
+                s_status[j] = cnt ? 2 : 1;
+                confl += cnt;
             }
             __syncthreads();
-            // undecided survivors in rank order (warp 0): accepted iff no earlier ACCEPTED
-            // survivor is within distance < d
+            P_TR(1)
+            // Parallel rounds: an undecided survivor is rejected as soon as one earlier
+            // conflicting survivor is accepted, accepted once all of them are rejected.  Long
+            // dependency chains are finished by warp 0 walking the undecided ones in rank order.
+            // A survivor is accepted iff no earlier ACCEPTED survivor conflicts with it.
+            for (int round = 0; round < 8; ++round) {
+                int undecided = 0;
+                for (uint32_t j = tid; j < S; j += blockDim.x) {
+                    if (s_status[j] != 2) continue;
+                    const uint32_t na = s_adjn[j];
+                    bool acc_nb = false, und_nb = false;
+                    if (na != 255) {
+                        for (uint32_t t = 0; t < na; ++t) {
+                            const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
+                            acc_nb |= sk == 1;
+                            und_nb |= sk == 2;
+                        }
+                    } else {
+                        const uint32_t vj = s_val[j];
+                        for (uint32_t k = 0; k < j; ++k) {
+                            if ((uint32_t)__popc(vj ^ s_val[k]) < a.d) {
+                                const uint8_t sk = s_status[k];
+                                acc_nb |= sk == 1;
+                                und_nb |= sk == 2;
+                            }
+                        }
+                    }
+                    // a status read in the same round may be stale (2): that only delays
+                    if (acc_nb) s_status[j] = 0;
+                    else if (!und_nb) s_status[j] = 1;
+                    else undecided = 1;
+                }
+                if (a.timing && tid == 0) atomicAdd(&st->n_rounds, 1ull);
+                if (!__syncthreads_or(undecided)) break;
+            }
             if (tid < 32) {
                 for (uint32_t j = 0; j < S; ++j) {
-                    if (s_status[j] != 2) continue;      // uniform across the warp
-                    const uint32_t vj = s_val[j];
-                    bool c = false;
-                    for (uint32_t k = lane; k < j; k += 32)
-                        c |= (s_status[k] == 1) && (uint32_t)__popc(vj ^ s_val[k]) < a.d;
-                    c = __any_sync(0xffffffffu, c);
-                    if (lane == 0) s_status[j] = c ? 0 : 1;
+                    if (s_status[j] != 2) continue;                 // warp-uniform
+                    if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
+                    const uint32_t na = s_adjn[j];
+                    bool acc_nb = false;
+                    if (na != 255) {
+                        if (lane < na) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
+                    } else {
+                        const uint32_t vj = s_val[j];
+                        for (uint32_t k = lane; k < j; k += 32)
+                            acc_nb |= (s_status[k] == 1) && (uint32_t)__popc(vj ^ s_val[k]) < a.d;
+                    }
+                    acc_nb = __any_sync(0xffffffffu, acc_nb);
+                    if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
                     __syncwarp();
                 }
             }
             __syncthreads();
+            P_TR(2)
             // ordered append
             const unsigned long long M0 = __ldcg(&st->M);
             uint32_t A = 0;
@@ -349,15 +439,31 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                 }
                 A += tot;
             }
+            P_TR(3)
             // clear per-tile state for the next tile
             for (uint32_t w = tid; w < kPMaxTile / 32; w += blockDim.x) a.dead[w] = 0;
             for (int l = 0; l < L; ++l)
                 for (uint32_t b = tid; b < kPMaxBatches; b += blockDim.x) st->bfin[l][b] = 0;
             for (int l = tid; l <= kPMaxLevels; l += blockDim.x) st->q_count[l] = 0;
-            if (rchk) atomicAdd(&st->resolve_checks, rchk);
-            if (confl) atomicAdd(&st->conflicts, confl);
-            if (wdef) atomicAdd(&st->w_def, wdef);
+            // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                rchk += __shfl_down_sync(0xffffffffu, rchk, o);
+                confl += __shfl_down_sync(0xffffffffu, confl, o);
+                wdef += __shfl_down_sync(0xffffffffu, wdef, o);
+            }
+            if (lane == 0) {
+                if (rchk) atomicAdd(&s_stat[0], rchk);
+                if (confl) atomicAdd(&s_stat[1], confl);
+                if (wdef) atomicAdd(&s_stat[2], wdef);
+            }
             __syncthreads();
+            if (tid == 0) {
+                st->resolve_checks += s_stat[0];
+                st->conflicts += s_stat[1];
+                st->w_def += s_stat[2];
+            }
+            P_TR(4)
             if (tid == 0) {
                 unsigned long long M1 = M0 + A;
                 if (M1 > a.capacity) M1 = a.capacity;
@@ -368,7 +474,9 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
             }
             __threadfence();
         }
+        if (timer) { const unsigned long long t = p_now(); st->t_resolve += t - tm; tm = t; }
         grid.sync();
+        if (timer) { const unsigned long long t = p_now(); st->t_sync += t - tm; st->t_tile += t - tm_tile; }
         t0 += K;
     }
     // work counter: lanes hold per-lane counts
@@ -456,10 +564,12 @@ int persistent_run(const RunArgs &r) {
     a.N = 1ull << r.n;
     a.tile_min = r.opt.tile_min; a.tile_max = r.opt.tile_max ? r.opt.tile_max : kPDefaultTile;
     a.W0 = r.opt.window0;
+    a.growth = (int)r.opt.growth;
     a.codebook = r.d_codebook; a.capacity = r.capacity;
     a.tabs = cx->tabs; a.vals = cx->vals; a.dead = cx->dead;
     a.q0 = cx->q0; a.q1 = cx->q1; a.surv = cx->surv; a.status = cx->status;
     a.st = cx->st; a.d_count = (unsigned long long *)r.d_count;
+    a.timing = getenv("GC_DEBUG_PHASES") != nullptr;
     int per_sm = 0;
     PCK(cudaFuncSetAttribute(k_construct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPDynSmem));
     PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_construct, kPThreads, kPDynSmem));
@@ -489,6 +599,22 @@ int persistent_run(const RunArgs &r) {
         o->launches = 1;
         o->screen_launches = 1;
         o->screen_ms = ms;
+        if (a.timing) {
+            PState full;
+            PCK(cudaMemcpy(&full, cx->st, offsetof(PState, q_count), cudaMemcpyDeviceToHost));
+            const double T = (double)full.tiles;
+            fprintf(stderr, "[gc] persistent: %llu tiles, per tile: total %.2f us, resolve %.2f us, final sync %.2f us\n",
+                    full.tiles, full.t_tile / T / 1e3, full.t_resolve / T / 1e3, full.t_sync / T / 1e3);
+            fprintf(stderr, "[gc]   resolve: gather %.2f conflicts %.2f sequential %.2f append %.2f clear+stats %.2f us\n",
+                    full.t_r[0] / T / 1e3, full.t_r[1] / T / 1e3, full.t_r[2] / T / 1e3, full.t_r[3] / T / 1e3,
+                    full.t_r[4] / T / 1e3);
+            fprintf(stderr, "[gc]   resolve: per tile %.2f adjacency overflows, %.2f rounds, %.2f sequential nodes\n",
+                    full.n_overflow / T, full.n_rounds / T, full.n_seq / T);
+            for (int l = 0; l < kPMaxLevels; ++l)
+                if (full.t_level[l])
+                    fprintf(stderr, "[gc]   level %2d: %.3f s total (%.2f us per tile)\n", l, full.t_level[l] / 1e9,
+                            full.t_level[l] / T / 1e3);
+        }
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }
     return GC_OK;

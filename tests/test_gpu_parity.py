@@ -178,6 +178,9 @@ SCHEDULES = [
     {"tile_max": 8192},                 # persistent kernel, largest tile
     {"tile_min": 32, "tile_max": 256, "window0": 64},
     {"tile_min": 1024, "tile_max": 1024, "window0": 1 << 14},
+    {"window_growth": 1},
+    {"window_growth": 4, "window0": 64},
+    {"flags": 16, "window_growth": 3, "window0": 128},
 ]
 
 
