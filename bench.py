@@ -206,15 +206,10 @@ def run_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n, d, o = parse_workload(args.workload)
+    from paper_1507_05398_b200 import dist as gdist
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(gc.gc_nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        comm = gc.gc_comm_create(bytes(idt.cpu().numpy().tobytes()), rank, world)
-    else:
-        comm = gc.gc_comm_create(None, 0, 1)
+    comm = gdist.comm_from_group()
 
     cap = gc.gc_capacity_bound(n, d)
     codebook = torch.empty(cap, dtype=torch.int32, device=dev)
@@ -249,10 +244,7 @@ def run_b200(args):
     barrier()
     sampler.stop()
     dev_ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = gdist.max_over_ranks(dev_ms) if world > 1 else dev_ms
     ms_per_step = max_ms / args.steps
     M = int(count.item())
     w_def = stats[-1]["w_def"]
@@ -292,9 +284,7 @@ def run_b200(args):
             tot += e0.elapsed_time(e1)
             if rank == 0:
                 d2h = host.numel() * 4 + 8
-        tt = torch.tensor([tot], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_val = w_def / (float(tt.item()) / args.steps * 1e-3)
+        e2e_val = w_def / (gdist.max_over_ranks(tot) / args.steps * 1e-3)
 
     # roofline of the dominant kernel (k_screen): executed checks / its summed device time
     checks = sum(s["checks_exec"] for s in stats)

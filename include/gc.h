@@ -70,7 +70,7 @@ typedef struct gc_options {
     uint32_t struct_size;
     uint32_t tile_min;       /* smallest candidate tile K (power of 2, >= 32), default 256              */
     uint32_t tile_max;       /* largest candidate tile K (power of 2, <= 2^20); default 4096 for the
-                                persistent kernel (which takes tiles <= 8192), 65536 for launched tiles */
+                                persistent kernel (which takes tiles <= 4096), 65536 for launched tiles */
     uint32_t window0;        /* first newest-first codebook window (power of 2), default 1024           */
     uint32_t emulate_ranks;  /* >1: split every tile's candidates into this many partitions on ONE GPU,
                                 exactly as gc_generate_rank splits them across GPUs (testing), default 1 */
@@ -188,6 +188,14 @@ int gc_comm_destroy(gc_comm *comm);   /* NULL is a no-op */
 int gc_generate_rank(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt,
                      gc_comm *comm, uint32_t *d_codebook, uint64_t capacity, uint64_t *d_count,
                      void *stream, gc_stats *stats);
+
+/* The candidate partition every rank uses inside a tile of K candidates (host-side, pure):
+ * the tile is padded to Kpad = ceil(K / (32 world)) * 32 world candidates (padding is
+ * never accepted) and rank r screens [r Kpad/world, (r+1) Kpad/world), a whole number of
+ * 32-bit mask words, so the all-gather of the mask words rebuilds the tile's mask in rank
+ * order.  GC_EINVAL for a bad world/rank or NULL outputs. */
+int gc_tile_partition(uint32_t K, int world, int rank, uint32_t *part_lo, uint32_t *part_len,
+                      uint32_t *Kpad);
 
 /* ------------------------------------------------------------------- misc */
 const char *gc_strerror(int status);

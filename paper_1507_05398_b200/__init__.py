@@ -40,6 +40,7 @@ from ._binding import (  # noqa: F401
     gc_ranks_to_vectors,
     gc_ranks_to_vectors_device,
     gc_strerror,
+    gc_tile_partition,
     gc_vector_to_rank,
     ordering_id,
 )

@@ -82,6 +82,7 @@ _sig("gc_generate_rank", ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, ctypes
                                         ctypes.POINTER(gc_options), ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.POINTER(gc_stats)])
+_sig("gc_tile_partition", ctypes.c_int, [ctypes.c_uint32, ctypes.c_int, ctypes.c_int, _u32p, _u32p, _u32p])
 _sig("gc_strerror", ctypes.c_char_p, [ctypes.c_int])
 _sig("gc_last_error", ctypes.c_char_p, [])
 _sig("gc_abi_version", ctypes.c_int, [])
@@ -211,6 +212,14 @@ def gc_ranks_to_vectors_device(ordering, n: int, first: int, count: int, out, st
     _check(_lib.gc_ranks_to_vectors_device(ordering_id(ordering), n, first, count, out.data_ptr(),
                                            _stream_ptr(stream)), "gc_ranks_to_vectors_device")
     return out
+
+
+def gc_tile_partition(K: int, world: int, rank: int) -> tuple[int, int, int]:
+    """(part_lo, part_len, Kpad) of `rank` inside a tile of K candidates."""
+    lo, ln, kp = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+    _check(_lib.gc_tile_partition(K, world, rank, ctypes.byref(lo), ctypes.byref(ln), ctypes.byref(kp)),
+           "gc_tile_partition")
+    return lo.value, ln.value, kp.value
 
 
 def gc_nccl_id_bytes() -> int:

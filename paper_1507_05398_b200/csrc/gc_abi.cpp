@@ -316,6 +316,21 @@ int gc_nccl_unique_id(uint8_t *id, size_t id_bytes) {
     return GC_OK;
 }
 
+int gc_tile_partition(uint32_t K, int world, int rank, uint32_t *part_lo, uint32_t *part_len, uint32_t *Kpad) {
+    clear_error();
+    if (!part_lo || !part_len || !Kpad) { set_error("NULL output"); return GC_EINVAL; }
+    if (world < 1 || world > 64 || (world & (world - 1)) || rank < 0 || rank >= world) {
+        set_error("world must be a power of two in [1, 64] and 0 <= rank < world");
+        return GC_EINVAL;
+    }
+    const uint32_t q = 32u * (uint32_t)world;
+    const uint32_t kp = (K + q - 1) / q * q;
+    *Kpad = kp;
+    *part_len = kp / (uint32_t)world;
+    *part_lo = (uint32_t)rank * (kp / (uint32_t)world);
+    return GC_OK;
+}
+
 struct gc_comm {
     int rank = 0, world = 1;
     void *nccl = nullptr;

@@ -566,9 +566,8 @@ int engine_run(const RunArgs &a) {
     while (t0 < N) {
         uint32_t K = tile_size(o, t0);
         if ((unsigned long long)K > N - t0) K = (uint32_t)(N - t0);
-        const uint32_t quantum = 32u * G;
-        const uint32_t Kpad = (K + quantum - 1) / quantum * quantum;
-        const uint32_t part = Kpad / G;
+        uint32_t Kpad = 0, part = 0, plo0 = 0;
+        if (gc_tile_partition(K, (int)G, 0, &plo0, &part, &Kpad) != GC_OK) return GC_EINTERNAL;
         // upper bound on M before this tile: last completed tile's M + ranks since
         // (multi-process: only the deterministic bound, so every rank launches the same
         // phases and the same collectives; the last phase always reaches codeword 0, so
@@ -592,7 +591,8 @@ int engine_run(const RunArgs &a) {
             cx->tabs, a.ordering, (int)a.n, t0, K, Kpad, cx->vals, cx->dead, cx->ctr);
         for (unsigned pl = 0; pl < parts_local; ++pl) {
             const unsigned g = (a.world > 1) ? (unsigned)a.rank : pl;
-            const uint32_t plo = g * part;
+            uint32_t plo = 0, plen = 0, kp = 0;
+            if (gc_tile_partition(K, (int)G, (int)g, &plo, &plen, &kp) != GC_OK) return GC_EINTERNAL;
             const uint2 *lin = nullptr;
             const unsigned int *cin = nullptr;
             for (int p = 0; p < P; ++p) {

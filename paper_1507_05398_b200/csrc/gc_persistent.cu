@@ -35,14 +35,13 @@ namespace gc {
 
 constexpr int kPThreads = 512;              // threads per CTA (16 warps); grid = #SMs
 constexpr int kPWarps = kPThreads / 32;
-constexpr int kPR = 2;                      // candidates per lane
-constexpr int kPBatch = 32 * kPR;           // candidates per warp item
+constexpr uint32_t kPR2Min = 1024;          // levels with >= this many candidates use 2 per lane
 constexpr uint32_t kPSubMin = 64;           // codewords per warp item: at least ...
 constexpr uint32_t kPSubMax = 2048;         // ... and at most
 constexpr int kPMaxLevels = 32;
-constexpr uint32_t kPMaxTile = 1u << 13;    // largest tile for this engine (survivors fit in smem)
-constexpr uint32_t kPMaxBatches = kPMaxTile / kPBatch;
-constexpr int kPAdj = 8;                        // earlier in-tile conflicts recorded per survivor
+constexpr uint32_t kPMaxTile = 1u << 12;    // largest tile for this engine (survivors fit in smem)
+constexpr uint32_t kPMaxBatches = kPMaxTile / 32;
+constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + s_adjn (1 B) + s_adj (2 B x kPAdj)
 constexpr size_t kPDynSmem = (size_t)kPMaxTile * (8 + 2 * kPAdj);
 
@@ -110,8 +109,9 @@ __device__ __forceinline__ int p_levels(unsigned long long M, uint32_t W0, int g
 // 128-byte load (lane k holds codeword top-1-k), prefetches the next block while it works
 // on this one, and broadcasts each codeword with a shuffle.  Early exit (warp vote) after
 // every block once every lane's candidates are dead.
+template <int R>
 __device__ __forceinline__ uint32_t p_scan(const uint32_t *__restrict__ cb, long long a, long long b,
-                                           uint32_t cur, const uint32_t (&v)[kPR], uint32_t (&m)[kPR],
+                                           uint32_t cur, const uint32_t (&v)[R], uint32_t (&m)[R],
                                            uint32_t d) {
     const int lane = threadIdx.x & 31;
     long long top = b;
@@ -125,20 +125,20 @@ __device__ __forceinline__ uint32_t p_scan(const uint32_t *__restrict__ cb, long
             for (int k = 0; k < 32; ++k) {
                 const uint32_t c = __shfl_sync(0xffffffffu, cur, k);
 #pragma unroll
-                for (int r = 0; r < kPR; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
+                for (int r = 0; r < R; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
             }
             scanned += 32;
         } else {
             for (int k = 0; k < (int)nv; ++k) {
                 const uint32_t c = __shfl_sync(0xffffffffu, cur, k);
 #pragma unroll
-                for (int r = 0; r < kPR; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
+                for (int r = 0; r < R; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
             }
             scanned += (uint32_t)nv;
         }
         bool done = true;
 #pragma unroll
-        for (int r = 0; r < kPR; ++r) done &= (m[r] < d);
+        for (int r = 0; r < R; ++r) done &= (m[r] < d);
         if (__all_sync(0xffffffffu, done)) break;
         cur = nxt;
         top = ntop;
@@ -172,6 +172,95 @@ __device__ __forceinline__ uint32_t p_block_scan(uint32_t x, uint32_t *total, ui
     *total = ws[32];
     __syncthreads();
     return r;
+}
+
+struct PLevel {
+    int l, L;
+    uint32_t n_l, B, nsub;
+    long long hi, lo, sub;
+    unsigned long long t0;
+    const uint2 *qin;
+    uint2 *qout;
+};
+
+// One warp item: batch b (32 R candidates) of the level's list against sub-range j of the
+// level's window.  The warp that completes the batch's last sub-range pushes its live
+// candidates to the next level's list.
+template <int R>
+__device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigned long long it,
+                                       const uint32_t (*C)[33], const uint64_t *off,
+                                       unsigned long long &my_checks) {
+    const int lane = threadIdx.x & 31;
+    PState *st = a.st;
+    const uint32_t j = (uint32_t)(it / lv.B), b = (uint32_t)(it % lv.B);
+    const long long s_hi = lv.hi - (long long)j * lv.sub;            // j = 0: newest
+    const long long s_lo = max(lv.lo, s_hi - lv.sub);
+    // first codeword block in flight while the candidates are fetched
+    const uint32_t cur0 = (s_hi - 1 - lane >= s_lo) ? __ldcg(a.codebook + s_hi - 1 - lane) : 0u;
+    uint32_t v[R], m[R], idx[R];
+    bool live[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t pos = b * (32u * R) + r * 32 + lane;
+        live[r] = pos < lv.n_l;
+        idx[r] = 0; v[r] = 0;
+        if (live[r]) {
+            if (lv.qin) { const uint2 e = __ldcg(lv.qin + pos); idx[r] = e.x; v[r] = e.y; }
+            else {
+                idx[r] = pos;
+                v[r] = rank_to_vector32(a.ord, a.n, C, off, lv.t0 + pos);
+                if (j == 0) a.vals[pos] = v[r];
+                // other sub-ranges of this level may already have killed it
+                if (lv.nsub > 1) live[r] = !((__ldcg(a.dead + (pos >> 5)) >> (pos & 31)) & 1u);
+            }
+        }
+        m[r] = live[r] ? 64u : 0u;
+    }
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) any |= live[r];
+    bool kill[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) kill[r] = false;
+    if (__any_sync(0xffffffffu, any)) {
+        const uint32_t sc = p_scan<R>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
+        my_checks += (unsigned long long)sc * R;   // per lane; summed over lanes at the end
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            kill[r] = live[r] && m[r] < a.d;
+            if (!lv.qin) {
+                const unsigned bb = __ballot_sync(0xffffffffu, kill[r]);
+                if (lane == 0 && bb) atomicOr(&a.dead[idx[r] >> 5], bb);
+            } else if (kill[r]) {
+                atomicOr(&a.dead[idx[r] >> 5], 1u << (idx[r] & 31));
+            }
+        }
+    }
+    if (lv.l + 1 < lv.L) {
+        unsigned last = 1;
+        if (lv.nsub > 1) {
+            __threadfence();
+            if (lane == 0) last = (atomicAdd(&st->bfin[lv.l][b], 1u) + 1u == lv.nsub);
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) __threadfence();
+        }
+        if (last) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t pos = b * (32u * R) + r * 32 + lane;
+                bool alive = pos < lv.n_l;
+                if (alive) {
+                    if (lv.nsub > 1) alive = !((__ldcg(a.dead + (idx[r] >> 5)) >> (idx[r] & 31)) & 1u);
+                    else alive = !kill[r];
+                }
+                const unsigned bb = __ballot_sync(0xffffffffu, alive);
+                unsigned base = 0;
+                if (lane == 0 && bb) base = atomicAdd(&st->q_count[lv.l + 1], (unsigned)__popc(bb));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (alive) lv.qout[base + __popc(bb & ((1u << lane) - 1u))] = make_uint2(idx[r], v[r]);
+            }
+        }
+    }
 }
 
 __device__ __forceinline__ unsigned long long p_now() {
@@ -221,7 +310,11 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
             const uint32_t n_l = (l == 0) ? K : __ldcg(&st->q_count[l]);
             const uint2 *qin = (l == 0) ? nullptr : ((l & 1) ? a.q1 : a.q0);
             uint2 *qout = (l & 1) ? a.q0 : a.q1;
-            const uint32_t B = (n_l + kPBatch - 1) / kPBatch;
+            // levels with few live candidates use 32-candidate batches (R = 1) so that partly
+            // filled batches waste fewer lanes; shallow levels use R = 2 (two checks per load)
+            const int R = (n_l >= kPR2Min) ? 2 : 1;
+            const uint32_t batch = 32u * R;
+            const uint32_t B = (n_l + batch - 1) / batch;
             // sub-ranges of the window, newest first, sized so the level has ~4 items per warp
             const long long wlen = hi - lo;
             long long sub = 0;
@@ -234,79 +327,14 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                 sub = min(sub, (long long)kPSubMax);
                 nsub = (uint32_t)((wlen + sub - 1) / sub);
             }
+            PLevel lv;
+            lv.l = l; lv.L = L; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
+            lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0;
+            lv.qin = qin; lv.qout = qout;
             const unsigned long long items = (unsigned long long)B * nsub;
             for (unsigned long long it = gwarp; it < items; it += nwarps) {
-                const uint32_t j = (uint32_t)(it / B), b = (uint32_t)(it % B);
-                const long long s_hi = hi - (long long)j * sub;            // j = 0: newest
-                const long long s_lo = max(lo, s_hi - sub);
-                // first codeword block in flight while the candidates are fetched
-                const uint32_t cur0 = (s_hi - 1 - lane >= s_lo) ? __ldcg(a.codebook + s_hi - 1 - lane) : 0u;
-                // candidates of batch b (level 0: generated from their ranks)
-                uint32_t v[kPR], m[kPR], idx[kPR];
-                bool live[kPR];
-#pragma unroll
-                for (int r = 0; r < kPR; ++r) {
-                    const uint32_t pos = b * kPBatch + r * 32 + lane;
-                    live[r] = pos < n_l;
-                    idx[r] = 0; v[r] = 0;
-                    if (live[r]) {
-                        if (qin) { const uint2 e = __ldcg(qin + pos); idx[r] = e.x; v[r] = e.y; }
-                        else {
-                            idx[r] = pos;
-                            v[r] = rank_to_vector32(a.ord, a.n, C, off, t0 + pos);
-                            if (j == 0) a.vals[pos] = v[r];
-                            // other sub-ranges of this level may already have killed it
-                            if (nsub > 1) live[r] = !((__ldcg(a.dead + (pos >> 5)) >> (pos & 31)) & 1u);
-                        }
-                    }
-                    m[r] = live[r] ? 64u : 0u;
-                }
-                bool any = false;
-#pragma unroll
-                for (int r = 0; r < kPR; ++r) any |= live[r];
-                bool kill[kPR];
-#pragma unroll
-                for (int r = 0; r < kPR; ++r) kill[r] = false;
-                if (__any_sync(0xffffffffu, any)) {
-                    const uint32_t sc = p_scan(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
-                    my_checks += (unsigned long long)sc * kPR;   // per lane; summed over lanes below
-#pragma unroll
-                    for (int r = 0; r < kPR; ++r) {
-                        kill[r] = live[r] && m[r] < a.d;
-                        if (!qin) {
-                            const unsigned bb = __ballot_sync(0xffffffffu, kill[r]);
-                            if (lane == 0 && bb) atomicOr(&a.dead[idx[r] >> 5], bb);
-                        } else if (kill[r]) {
-                            atomicOr(&a.dead[idx[r] >> 5], 1u << (idx[r] & 31));
-                        }
-                    }
-                }
-                if (l + 1 < L) {
-                    // the warp finishing batch b's last item pushes its live candidates
-                    unsigned last = 1;
-                    if (nsub > 1) {
-                        __threadfence();
-                        if (lane == 0) last = (atomicAdd(&st->bfin[l][b], 1u) + 1u == nsub);
-                        last = __shfl_sync(0xffffffffu, last, 0);
-                        if (last) __threadfence();
-                    }
-                    if (last) {
-#pragma unroll
-                        for (int r = 0; r < kPR; ++r) {
-                            const uint32_t pos = b * kPBatch + r * 32 + lane;
-                            bool alive = pos < n_l;
-                            if (alive) {
-                                if (nsub > 1) alive = !((__ldcg(a.dead + (idx[r] >> 5)) >> (idx[r] & 31)) & 1u);
-                                else alive = !kill[r];
-                            }
-                            const unsigned bb = __ballot_sync(0xffffffffu, alive);
-                            unsigned base = 0;
-                            if (lane == 0 && bb) base = atomicAdd(&st->q_count[l + 1], (unsigned)__popc(bb));
-                            base = __shfl_sync(0xffffffffu, base, 0);
-                            if (alive) qout[base + __popc(bb & ((1u << lane) - 1u))] = make_uint2(idx[r], v[r]);
-                        }
-                    }
-                }
+                if (R == 2) p_item<2>(a, lv, it, C, off, my_checks);
+                else p_item<1>(a, lv, it, C, off, my_checks);
             }
             grid.sync();
             if (timer) { const unsigned long long t = p_now(); st->t_level[l] += t - tm; tm = t; }
@@ -373,6 +401,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
             // conflicting survivor is accepted, accepted once all of them are rejected.  Long
             // dependency chains are finished by warp 0 walking the undecided ones in rank order.
             // A survivor is accepted iff no earlier ACCEPTED survivor conflicts with it.
+            int left = 0;
             for (int round = 0; round < 8; ++round) {
                 int undecided = 0;
                 for (uint32_t j = tid; j < S; j += blockDim.x) {
@@ -401,9 +430,10 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                     else undecided = 1;
                 }
                 if (a.timing && tid == 0) atomicAdd(&st->n_rounds, 1ull);
-                if (!__syncthreads_or(undecided)) break;
+                left = __syncthreads_or(undecided);
+                if (!left) break;
             }
-            if (tid < 32) {
+            if (left && tid < 32) {
                 for (uint32_t j = 0; j < S; ++j) {
                     if (s_status[j] != 2) continue;                 // warp-uniform
                     if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);

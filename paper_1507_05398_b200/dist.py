@@ -1,0 +1,46 @@
+"""Process-group plumbing for the multi-GPU construction (one process per GPU).
+
+Only plumbing lives here (PyTorch is used for process groups, not for compute):
+  share_nccl_id  -- rank 0 creates the NCCL unique id, every rank receives the bytes
+  max_over_ranks -- the max of a per-rank number (timing: max over ranks)
+  comm_from_group -- a gc_comm for this rank (world 1: no NCCL)
+The construction itself is gc_generate_rank (libgc.so).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _binding as B
+
+
+def _device_for(group=None):
+    backend = dist.get_backend(group)
+    return torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+
+
+def share_nccl_id(group=None, make_id=None) -> bytes:
+    """Rank 0's fresh NCCL unique id (gc_nccl_unique_id), broadcast to every rank."""
+    make_id = make_id or B.gc_nccl_unique_id
+    dev = _device_for(group)
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if dist.get_rank(group) == 0:
+        t.copy_(torch.frombuffer(bytearray(make_id()), dtype=torch.uint8))
+    dist.broadcast(t, src=0, group=group)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def max_over_ranks(x: float, group=None) -> float:
+    dev = _device_for(group)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def comm_from_group(group=None):
+    """gc_comm for this process: NCCL over `world` ranks (world 1: no NCCL)."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world == 1:
+        return B.gc_comm_create(None, 0, 1)
+    return B.gc_comm_create(share_nccl_id(group), rank, world)

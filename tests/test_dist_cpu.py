@@ -1,0 +1,86 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the N>1 host logic: NCCL-id sharing,
+max-over-ranks timing, and the tile partition every rank derives independently (it
+must tile [0, Kpad) exactly, in rank order, in whole mask words)."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1507_05398_b200 as gc
+        from paper_1507_05398_b200 import dist as gdist
+
+        out = {}
+        ident = gdist.share_nccl_id()
+        out["id"] = ident
+        out["max"] = gdist.max_over_ranks(10.0 + rank)
+        parts = {}
+        for K in (1, 7, 32, 33, 64, 256, 4096, 4097, 65536):
+            parts[K] = gc.gc_tile_partition(K, world, rank)
+        out["parts"] = parts
+        # every rank's (lo, len) gathered: must be identical lengths and contiguous
+        t = torch.tensor([parts[4097][0], parts[4097][1]], dtype=torch.int64)
+        gathered = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        out["gathered"] = [tuple(g.tolist()) for g in gathered]
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_host_logic():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0]["id"] == res[1]["id"] and len(res[0]["id"]) == 128
+    assert res[0]["max"] == res[1]["max"] == 11.0
+    for K, (lo0, ln0, kp0) in res[0]["parts"].items():
+        lo1, ln1, kp1 = res[1]["parts"][K]
+        assert kp0 == kp1 >= K and kp0 % (32 * world) == 0
+        assert ln0 == ln1 == kp0 // world and ln0 % 32 == 0
+        assert lo0 == 0 and lo1 == ln0                 # rank order, contiguous, disjoint
+    assert res[0]["gathered"] == res[1]["gathered"]
+    assert [g[0] for g in res[0]["gathered"]] == [0, res[0]["gathered"][0][1]]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8, 64])
+def test_partition_covers_tile(world):
+    import paper_1507_05398_b200 as gc
+    for K in (1, 31, 32, 100, 4096, 8191, 65536):
+        covered = []
+        for r in range(world):
+            lo, ln, kp = gc.gc_tile_partition(K, world, r)
+            covered.extend(range(lo, lo + ln))
+            assert lo % 32 == 0 and ln % 32 == 0
+        assert covered == list(range(kp)) and kp >= K and kp - K < 32 * world
+
+
+def test_partition_rejects_bad_args():
+    import paper_1507_05398_b200 as gc
+    for world, rank in ((3, 0), (2, 2), (0, 0), (128, 0), (2, -1)):
+        with pytest.raises(gc.GCError):
+            gc.gc_tile_partition(64, world, rank)

@@ -175,7 +175,7 @@ SCHEDULES = [
     {"emulate_ranks": 4, "flags": 1},
     {"flags": 16},                      # host-launched tiles (default 65536)
     {"flags": 16, "tile_max": 4096, "window0": 256},
-    {"tile_max": 8192},                 # persistent kernel, largest tile
+    {"tile_max": 8192},                 # beyond the persistent kernel's tiles: launched engine
     {"tile_min": 32, "tile_max": 256, "window0": 64},
     {"tile_min": 1024, "tile_max": 1024, "window0": 1 << 14},
     {"window_growth": 1},
