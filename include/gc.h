@@ -69,9 +69,10 @@ typedef enum gc_status {
 typedef struct gc_options {
     uint32_t struct_size;
     uint32_t tile_min;       /* smallest candidate tile K (power of 2, >= 32), default 256              */
-    uint32_t tile_max;       /* largest candidate tile K (power of 2, <= 2^20); default 4096 for the
-                                persistent kernel (which takes tiles <= 4096), 65536 for launched tiles */
-    uint32_t window0;        /* first newest-first codebook window (power of 2), default 1024           */
+    uint32_t tile_max;       /* largest candidate tile K (power of 2, <= 2^20), default 65536; the
+                                persistent kernel (tiles <= 65536) sizes tiles adaptively for ~128
+                                accepted words per tile                                          */
+    uint32_t window0;        /* first newest-first codebook window (power of 2), default 4096           */
     uint32_t emulate_ranks;  /* >1: split every tile's candidates into this many partitions on ONE GPU,
                                 exactly as gc_generate_rank splits them across GPUs (testing), default 1 */
     uint32_t flags;          /* GC_FLAG_* below                                                          */
@@ -85,6 +86,8 @@ typedef struct gc_options {
 #define GC_FLAG_LAUNCHED_TILES 0x10u /* host-launched tile kernels instead of the persistent
                                         device-resident construction kernel (the multi-GPU and
                                         emulate_ranks paths always use them)                      */
+#define GC_FLAG_POPC_ONLY      0x20u /* every check by XOR+POPC (default for d <= 4: half of them
+                                        by an ALU bit-clearing test of the same predicate)         */
 #define GC_FLAG_KERNEL_TIMING  0x8u  /* bracket every screen launch with CUDA events on the launching
                                         stream; fills gc_stats.screen_ms (benchmarking)               */
 

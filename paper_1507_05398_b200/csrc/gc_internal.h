@@ -18,7 +18,7 @@ void clear_error();
 struct Options {
     uint32_t tile_min = 256;
     uint32_t tile_max = 0;          // 0 = engine default (persistent 4096, launched 65536)
-    uint32_t window0 = 1024;
+    uint32_t window0 = 4096;
     uint32_t emulate_ranks = 1;
     uint32_t flags = 0;
     uint32_t growth = 2;            // log2 window growth per level

@@ -35,15 +35,17 @@ namespace gc {
 
 constexpr int kPThreads = 512;              // threads per CTA (16 warps); grid = #SMs
 constexpr int kPWarps = kPThreads / 32;
-constexpr uint32_t kPR2Min = 1024;          // levels with >= this many candidates use 2 per lane
+constexpr uint32_t kPR2Min = 0;             // levels with >= this many candidates use 2 per lane
 constexpr uint32_t kPSubMin = 64;           // codewords per warp item: at least ...
 constexpr uint32_t kPSubMax = 2048;         // ... and at most
 constexpr int kPMaxLevels = 32;
-constexpr uint32_t kPMaxTile = 1u << 12;    // largest tile for this engine (survivors fit in smem)
+constexpr uint32_t kPMaxTile = 1u << 16;    // largest tile (tile indices fit in 16 bits)
+constexpr uint32_t kPChunk = 1u << 12;      // survivors resolved per chunk (shared memory)
 constexpr uint32_t kPMaxBatches = kPMaxTile / 32;
+constexpr uint32_t kPTargetAccepted = 128;  // adaptive tiles grow up to ~2x this many accepted words
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + s_adjn (1 B) + s_adj (2 B x kPAdj)
-constexpr size_t kPDynSmem = (size_t)kPMaxTile * (8 + 2 * kPAdj);
+constexpr size_t kPDynSmem = (size_t)kPChunk * (8 + 2 * kPAdj);
 
 struct PState {
     unsigned long long M;
@@ -59,6 +61,7 @@ struct PState {
     unsigned long long t_r[6];                 // resolve sub-steps
     unsigned long long n_overflow, n_seq, n_rounds;
     unsigned int error;
+    unsigned int K_next;                       // size of the next tile (set by CTA 0)
     unsigned int q_count[kPMaxLevels + 1];
     unsigned int bfin[kPMaxLevels][kPMaxBatches];
 };
@@ -69,6 +72,7 @@ struct PArgs {
     unsigned long long N;           // 2^n
     uint32_t tile_min, tile_max, W0;
     int growth;
+    int mix;                        // 2..4: half the checks via p_clear_low<d> (d <= 4), 0: POPC only
     uint32_t *codebook;
     unsigned long long capacity;
     const OrderTables *tabs;
@@ -82,11 +86,25 @@ struct PArgs {
     int timing;
 };
 
-__device__ __forceinline__ uint32_t p_tile_size(const PArgs &a, unsigned long long t0) {
-    uint32_t K = a.tile_min;
-    while (K < a.tile_max && (unsigned long long)K * 8 <= t0) K <<= 1;
-    if ((unsigned long long)K > a.N - t0) K = (uint32_t)(a.N - t0);
-    return K;
+// Next tile size (a power of two in [tile_min, tile_max]) after a tile of K candidates
+// with S survivors and A accepted, the construction now at rank t1 with M1 words.
+//   cap: the density seen so far (M1 / t1) predicts ~kPTargetAccepted accepted words per
+//        tile of size cap (sparse codes get long tiles, so little per-tile latency); also
+//        cap <= t1/8 while the history is short;
+//   K halves when false survivors (S - A) exceed A/4 -- each scans the whole codebook --
+//   and grows back toward cap while S <= 9/8 A.
+// Deterministic: a function of (K, S, A, t1, M1) only, never of timing.
+__device__ __forceinline__ uint32_t p_next_tile(const PArgs &a, uint32_t K, uint32_t S, uint32_t A,
+                                                unsigned long long t1, unsigned long long M1) {
+    const unsigned long long want = M1 ? (unsigned long long)kPTargetAccepted * t1 / M1 : ~0ull;
+    uint32_t cap = a.tile_min;
+    while (cap < a.tile_max && (unsigned long long)cap * 2 <= want && (unsigned long long)cap * 16 <= t1) cap <<= 1;
+    uint32_t Kn = K;
+    if (A > 0 && (unsigned long long)S * 4 > (unsigned long long)A * 5) Kn = K > a.tile_min ? K / 2 : K;
+    else if (A == 0 || (unsigned long long)S * 8 <= (unsigned long long)A * 9) Kn = K * 2;
+    if (Kn > cap) Kn = cap;
+    if (Kn < a.tile_min) Kn = a.tile_min;
+    return Kn;
 }
 
 // newest-first depth covered by levels 0 .. l-1: W0 (1 + g + ... + g^(l-1)), g = 2^growth
@@ -104,12 +122,36 @@ __device__ __forceinline__ int p_levels(unsigned long long M, uint32_t W0, int g
     return L;
 }
 
-// scan codewords [a, b) newest first for the lane's kPR candidates; returns the number of
+// x with its lowest D-1 set bits cleared: zero iff popc(x) < D (D - 1 applications of
+// x & (x - 1)).  Runs on the integer ALU/FMA pipes instead of the POPC unit.
+template <int D>
+__device__ __forceinline__ uint32_t p_clear_low(uint32_t x) {
+#pragma unroll
+    for (int i = 0; i < D - 1; ++i) x &= x - 1u;
+    return x;
+}
+
+// One candidate-codeword check, accumulated into m.  MIX = 0: m = min popc(v ^ c) (the
+// candidate dies when m < d).  MIX = D (2..4) for odd r: m = min p_clear_low<D>(v ^ c),
+// dies when m == 0 -- the same predicate popc(v ^ c) < d, evaluated without POPC so that
+// the two halves of a warp's checks use different pipes.
+template <int MIX>
+__device__ __forceinline__ void p_check(uint32_t &m, uint32_t v, uint32_t c, int r) {
+    if (MIX && (r & 1)) m = min(m, p_clear_low<MIX>(v ^ c));
+    else m = min(m, (uint32_t)__popc(v ^ c));
+}
+
+template <int MIX>
+__device__ __forceinline__ bool p_dead(uint32_t m, uint32_t d, int r) {
+    return (MIX && (r & 1)) ? (m == 0) : (m < d);
+}
+
+// scan codewords [a, b) newest first for the lane's R candidates; returns the number of
 // codewords scanned (for the work counter).  The warp reads 32 codewords per coalesced
 // 128-byte load (lane k holds codeword top-1-k), prefetches the next block while it works
 // on this one, and broadcasts each codeword with a shuffle.  Early exit (warp vote) after
 // every block once every lane's candidates are dead.
-template <int R>
+template <int R, int MIX>
 __device__ __forceinline__ uint32_t p_scan(const uint32_t *__restrict__ cb, long long a, long long b,
                                            uint32_t cur, const uint32_t (&v)[R], uint32_t (&m)[R],
                                            uint32_t d) {
@@ -125,20 +167,20 @@ __device__ __forceinline__ uint32_t p_scan(const uint32_t *__restrict__ cb, long
             for (int k = 0; k < 32; ++k) {
                 const uint32_t c = __shfl_sync(0xffffffffu, cur, k);
 #pragma unroll
-                for (int r = 0; r < R; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
+                for (int r = 0; r < R; ++r) p_check<MIX>(m[r], v[r], c, r);
             }
             scanned += 32;
         } else {
             for (int k = 0; k < (int)nv; ++k) {
                 const uint32_t c = __shfl_sync(0xffffffffu, cur, k);
 #pragma unroll
-                for (int r = 0; r < R; ++r) m[r] = min(m[r], (uint32_t)__popc(v[r] ^ c));
+                for (int r = 0; r < R; ++r) p_check<MIX>(m[r], v[r], c, r);
             }
             scanned += (uint32_t)nv;
         }
         bool done = true;
 #pragma unroll
-        for (int r = 0; r < R; ++r) done &= (m[r] < d);
+        for (int r = 0; r < R; ++r) done &= p_dead<MIX>(m[r], d, r);
         if (__all_sync(0xffffffffu, done)) break;
         cur = nxt;
         top = ntop;
@@ -186,7 +228,7 @@ struct PLevel {
 // One warp item: batch b (32 R candidates) of the level's list against sub-range j of the
 // level's window.  The warp that completes the batch's last sub-range pushes its live
 // candidates to the next level's list.
-template <int R>
+template <int R, int MIX>
 __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigned long long it,
                                        const uint32_t (*C)[33], const uint64_t *off,
                                        unsigned long long &my_checks) {
@@ -214,7 +256,7 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                 if (lv.nsub > 1) live[r] = !((__ldcg(a.dead + (pos >> 5)) >> (pos & 31)) & 1u);
             }
         }
-        m[r] = live[r] ? 64u : 0u;
+        m[r] = live[r] ? 0xffffffffu : 0u;      // dead lanes start "already dead" in both forms
     }
     bool any = false;
 #pragma unroll
@@ -223,11 +265,11 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
 #pragma unroll
     for (int r = 0; r < R; ++r) kill[r] = false;
     if (__any_sync(0xffffffffu, any)) {
-        const uint32_t sc = p_scan<R>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
+        const uint32_t sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
         my_checks += (unsigned long long)sc * R;   // per lane; summed over lanes at the end
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            kill[r] = live[r] && m[r] < a.d;
+            kill[r] = live[r] && p_dead<MIX>(m[r], a.d, r);
             if (!lv.qin) {
                 const unsigned bb = __ballot_sync(0xffffffffu, kill[r]);
                 if (lane == 0 && bb) atomicOr(&a.dead[idx[r] >> 5], bb);
@@ -276,10 +318,10 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
     __shared__ uint32_t s_ws[33];
     extern __shared__ __align__(16) uint8_t p_dyn[];        // resolve scratch (kPDynSmem bytes)
     uint32_t *s_val = reinterpret_cast<uint32_t *>(p_dyn);
-    uint16_t *s_idx = reinterpret_cast<uint16_t *>(p_dyn + kPMaxTile * 4);
-    uint8_t *s_status = p_dyn + kPMaxTile * 6;
-    uint8_t *s_adjn = p_dyn + kPMaxTile * 7;
-    uint16_t *s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPMaxTile * 8);
+    uint16_t *s_idx = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 4);
+    uint8_t *s_status = p_dyn + kPChunk * 6;
+    uint8_t *s_adjn = p_dyn + kPChunk * 7;
+    uint16_t *s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 8);
     PState *st = a.st;
     const bool graded = a.ord >= GRADED_LEX;
     if (graded) {
@@ -294,8 +336,9 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
 
     unsigned long long t0 = 0;
     while (t0 < a.N) {
-        const uint32_t K = p_tile_size(a, t0);
         const unsigned long long M = __ldcg(&st->M);
+        uint32_t K = __ldcg(&st->K_next);
+        if ((unsigned long long)K > a.N - t0) K = (uint32_t)(a.N - t0);
         const int L = p_levels(M, a.W0, a.growth);
         const uint32_t W0 = a.W0;
         const bool timer = a.timing && blockIdx.x == 0 && threadIdx.x == 0;
@@ -333,8 +376,16 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
             lv.qin = qin; lv.qout = qout;
             const unsigned long long items = (unsigned long long)B * nsub;
             for (unsigned long long it = gwarp; it < items; it += nwarps) {
-                if (R == 2) p_item<2>(a, lv, it, C, off, my_checks);
-                else p_item<1>(a, lv, it, C, off, my_checks);
+                if (R == 2) {
+                    switch (a.mix) {
+                        case 2: p_item<2, 2>(a, lv, it, C, off, my_checks); break;
+                        case 3: p_item<2, 3>(a, lv, it, C, off, my_checks); break;
+                        case 4: p_item<2, 4>(a, lv, it, C, off, my_checks); break;
+                        default: p_item<2, 0>(a, lv, it, C, off, my_checks); break;
+                    }
+                } else {
+                    p_item<1, 0>(a, lv, it, C, off, my_checks);
+                }
             }
             grid.sync();
             if (timer) { const unsigned long long t = p_now(); st->t_level[l] += t - tm; tm = t; }
@@ -348,7 +399,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                 for (uint32_t i = tid; i < K; i += blockDim.x) a.vals[i] = rank_to_vector32(a.ord, a.n, C, off, t0 + i);
                 __syncthreads();
             }
-            // survivors in rank order -> s_val / s_idx
+            // survivors in rank order -> a.surv (global; S <= K)
             uint32_t S = 0;
             for (uint32_t w0 = 0; w0 < words; w0 += blockDim.x) {
                 const uint32_t w = w0 + tid;
@@ -363,9 +414,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                     const int bit = __ffs(alive) - 1;
                     alive &= alive - 1;
                     const uint32_t i = w * 32 + bit;
-                    s_idx[pos] = (uint16_t)i;
-                    s_val[pos] = __ldcg(a.vals + i);
-                    ++pos;
+                    a.surv[pos++] = make_uint2(i, __ldcg(a.vals + i));
                 }
                 S += tot;
             }
@@ -373,107 +422,122 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
             unsigned long long tr = timer ? p_now() : 0;
 #define P_TR(i) if (timer) { const unsigned long long t_ = p_now(); st->t_r[i] += t_ - tr; tr = t_; }
             if (timer) st->t_r[0] += tr - tm;
-            // in-tile conflicts: s_adj[j] lists (up to kPAdj) earlier survivors within distance
-            // < d of survivor j (s_adjn = 255: more than kPAdj).  status 1 = accepted,
-            // 0 = rejected, 2 = undecided.
             __shared__ unsigned long long s_stat[3];
             if (tid < 3) s_stat[tid] = 0;
             __syncthreads();
-            unsigned long long rchk = 0, confl = 0;
-            for (uint32_t j = tid; j < S; j += blockDim.x) {
-                const uint32_t vj = s_val[j];
-                uint32_t cnt = 0;
-                for (uint32_t k = 0; k < j; ++k) {
-                    if ((uint32_t)__popc(vj ^ s_val[k]) < a.d) {
-                        if (cnt < kPAdj) s_adj[j * kPAdj + cnt] = (uint16_t)k;
-                        ++cnt;
-                    }
+            unsigned long long rchk = 0, confl = 0, wdef = 0;
+            const unsigned long long M0 = __ldcg(&st->M);
+            uint32_t A = 0;                   // accepted so far in this tile (codebook[M0, M0+A))
+            for (uint32_t c0 = 0; c0 < S; c0 += kPChunk) {
+                const uint32_t Sc = min(kPChunk, S - c0);
+                for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                    const uint2 e = __ldcg(a.surv + c0 + j);
+                    s_idx[j] = (uint16_t)e.x;
+                    s_val[j] = e.y;
                 }
-                rchk += j;
-                s_adjn[j] = cnt > kPAdj ? 255 : (uint8_t)cnt;
-                if (a.timing && cnt > kPAdj) atomicAdd(&st->n_overflow, 1ull);
-                s_status[j] = cnt ? 2 : 1;
-                confl += cnt;
-            }
-            __syncthreads();
-            P_TR(1)
-            // Parallel rounds: an undecided survivor is rejected as soon as one earlier
-            // conflicting survivor is accepted, accepted once all of them are rejected.  Long
-            // dependency chains are finished by warp 0 walking the undecided ones in rank order.
-            // A survivor is accepted iff no earlier ACCEPTED survivor conflicts with it.
-            int left = 0;
-            for (int round = 0; round < 8; ++round) {
-                int undecided = 0;
-                for (uint32_t j = tid; j < S; j += blockDim.x) {
-                    if (s_status[j] != 2) continue;
-                    const uint32_t na = s_adjn[j];
-                    bool acc_nb = false, und_nb = false;
-                    if (na != 255) {
-                        for (uint32_t t = 0; t < na; ++t) {
-                            const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
-                            acc_nb |= sk == 1;
-                            und_nb |= sk == 2;
+                __syncthreads();
+                // in-chunk conflicts: s_adj[j] lists (up to kPAdj) earlier survivors of the chunk
+                // within distance < d (s_adjn = 255: more); survivors conflicting with a word
+                // accepted in an earlier chunk of this tile are rejected outright.
+                // status 1 = accepted, 0 = rejected, 2 = undecided.
+                for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                    const uint32_t vj = s_val[j];
+                    bool prev = false;
+                    for (uint32_t t = 0; t < A && !prev; ++t)
+                        prev = (uint32_t)__popc(vj ^ __ldcg(a.codebook + M0 + t)) < a.d;
+                    uint32_t cnt = 0;
+                    for (uint32_t k = 0; k < j; ++k) {
+                        if ((uint32_t)__popc(vj ^ s_val[k]) < a.d) {
+                            if (cnt < kPAdj) s_adj[j * kPAdj + cnt] = (uint16_t)k;
+                            ++cnt;
                         }
-                    } else {
-                        const uint32_t vj = s_val[j];
-                        for (uint32_t k = 0; k < j; ++k) {
-                            if ((uint32_t)__popc(vj ^ s_val[k]) < a.d) {
-                                const uint8_t sk = s_status[k];
+                    }
+                    rchk += j + A;
+                    s_adjn[j] = cnt > kPAdj ? 255 : (uint8_t)cnt;
+                    if (a.timing && cnt > kPAdj) atomicAdd(&st->n_overflow, 1ull);
+                    s_status[j] = prev ? 0 : (cnt ? 2 : 1);
+                    confl += cnt;
+                }
+                __syncthreads();
+                P_TR(1)
+                // Parallel rounds: an undecided survivor is rejected as soon as one earlier
+                // conflicting survivor is accepted, accepted once all of them are rejected.  Long
+                // dependency chains are finished by warp 0 walking the undecided ones in rank
+                // order.  A survivor is accepted iff no earlier ACCEPTED survivor conflicts.
+                int left = 0;
+                for (int round = 0; round < 8; ++round) {
+                    int undecided = 0;
+                    for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                        if (s_status[j] != 2) continue;
+                        const uint32_t na = s_adjn[j];
+                        bool acc_nb = false, und_nb = false;
+                        if (na != 255) {
+                            for (uint32_t t = 0; t < na; ++t) {
+                                const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
                                 acc_nb |= sk == 1;
                                 und_nb |= sk == 2;
                             }
+                        } else {
+                            const uint32_t vj = s_val[j];
+                            for (uint32_t k = 0; k < j; ++k) {
+                                if ((uint32_t)__popc(vj ^ s_val[k]) < a.d) {
+                                    const uint8_t sk = s_status[k];
+                                    acc_nb |= sk == 1;
+                                    und_nb |= sk == 2;
+                                }
+                            }
                         }
+                        // a status read in the same round may be stale (2): that only delays
+                        if (acc_nb) s_status[j] = 0;
+                        else if (!und_nb) s_status[j] = 1;
+                        else undecided = 1;
                     }
-                    // a status read in the same round may be stale (2): that only delays
-                    if (acc_nb) s_status[j] = 0;
-                    else if (!und_nb) s_status[j] = 1;
-                    else undecided = 1;
+                    if (a.timing && tid == 0) atomicAdd(&st->n_rounds, 1ull);
+                    left = __syncthreads_or(undecided);
+                    if (!left) break;
                 }
-                if (a.timing && tid == 0) atomicAdd(&st->n_rounds, 1ull);
-                left = __syncthreads_or(undecided);
-                if (!left) break;
-            }
-            if (left && tid < 32) {
-                for (uint32_t j = 0; j < S; ++j) {
-                    if (s_status[j] != 2) continue;                 // warp-uniform
-                    if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
-                    const uint32_t na = s_adjn[j];
-                    bool acc_nb = false;
-                    if (na != 255) {
-                        if (lane < na) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
-                    } else {
-                        const uint32_t vj = s_val[j];
-                        for (uint32_t k = lane; k < j; k += 32)
-                            acc_nb |= (s_status[k] == 1) && (uint32_t)__popc(vj ^ s_val[k]) < a.d;
+                if (left && tid < 32) {
+                    for (uint32_t j = 0; j < Sc; ++j) {
+                        if (s_status[j] != 2) continue;                 // warp-uniform
+                        if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
+                        const uint32_t na = s_adjn[j];
+                        bool acc_nb = false;
+                        if (na != 255) {
+                            if (lane < na) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
+                        } else {
+                            const uint32_t vj = s_val[j];
+                            for (uint32_t k = lane; k < j; k += 32)
+                                acc_nb |= (s_status[k] == 1) && (uint32_t)__popc(vj ^ s_val[k]) < a.d;
+                        }
+                        acc_nb = __any_sync(0xffffffffu, acc_nb);
+                        if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
+                        __syncwarp();
                     }
-                    acc_nb = __any_sync(0xffffffffu, acc_nb);
-                    if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
-                    __syncwarp();
                 }
-            }
-            __syncthreads();
-            P_TR(2)
-            // ordered append
-            const unsigned long long M0 = __ldcg(&st->M);
-            uint32_t A = 0;
-            unsigned long long wdef = 0;
-            for (uint32_t j0 = 0; j0 < S; j0 += blockDim.x) {
-                const uint32_t j = j0 + tid;
-                const uint32_t acc = (j < S && s_status[j] == 1) ? 1u : 0u;
-                uint32_t tot;
-                const uint32_t pos = A + p_block_scan(acc, &tot, s_ws);
-                if (acc) {
-                    if (M0 + pos < a.capacity) a.codebook[M0 + pos] = s_val[j];
-                    else st->error = 1;
-                    wdef += a.N - 1 - (t0 + s_idx[j]);
+                __syncthreads();
+                P_TR(2)
+                // ordered append of the chunk's accepted survivors
+                for (uint32_t j0 = 0; j0 < Sc; j0 += blockDim.x) {
+                    const uint32_t j = j0 + tid;
+                    const uint32_t acc = (j < Sc && s_status[j] == 1) ? 1u : 0u;
+                    uint32_t tot;
+                    const uint32_t pos = A + p_block_scan(acc, &tot, s_ws);
+                    if (acc) {
+                        if (M0 + pos < a.capacity) a.codebook[M0 + pos] = s_val[j];
+                        else st->error = 1;
+                        wdef += a.N - 1 - (t0 + s_idx[j]);
+                    }
+                    A += tot;
                 }
-                A += tot;
+                if (A > a.capacity - M0) A = (uint32_t)(a.capacity - M0);
+                __threadfence_block();
+                __syncthreads();
+                P_TR(3)
             }
-            P_TR(3)
             // clear per-tile state for the next tile
-            for (uint32_t w = tid; w < kPMaxTile / 32; w += blockDim.x) a.dead[w] = 0;
+            for (uint32_t w = tid; w < words; w += blockDim.x) a.dead[w] = 0;
             for (int l = 0; l < L; ++l)
-                for (uint32_t b = tid; b < kPMaxBatches; b += blockDim.x) st->bfin[l][b] = 0;
+                for (uint32_t b = tid; b < (K + 31) / 32; b += blockDim.x) st->bfin[l][b] = 0;
             for (int l = tid; l <= kPMaxLevels; l += blockDim.x) st->q_count[l] = 0;
             // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
 #pragma unroll
@@ -498,6 +562,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                 unsigned long long M1 = M0 + A;
                 if (M1 > a.capacity) M1 = a.capacity;
                 st->M = M1;
+                st->K_next = p_next_tile(a, K, S, A, t0 + K, M1);
                 st->survivors += S;
                 st->tiles += 1;
                 st->levels += L;
@@ -565,11 +630,10 @@ static int p_context(int device, PContext **out) {
     return GC_OK;
 }
 
-constexpr uint32_t kPDefaultTile = 4096;
+constexpr uint32_t kPDefaultTile = kPMaxTile;   // adaptive tiles up to this size
 
 bool persistent_supported(const RunArgs &a) {
     return a.world == 1 && a.opt.emulate_ranks == 1 && a.opt.tile_max <= kPMaxTile &&
-           a.opt.tile_min <= std::max(a.opt.tile_max, kPDefaultTile) &&
            !(a.opt.flags & (GC_FLAG_NO_EARLY_EXIT | GC_FLAG_FORCE_SEQ_RESOLVE | GC_FLAG_LAUNCHED_TILES));
 }
 
@@ -588,13 +652,20 @@ int persistent_run(const RunArgs &r) {
         cx->tabs_n = (int)r.n;
     }
     PCK(cudaMemsetAsync(cx->st, 0, sizeof(PState), s));
+    {
+        const uint32_t k0 = std::min<uint32_t>(r.opt.tile_min, r.opt.tile_max ? r.opt.tile_max : kPDefaultTile);
+        PCK(cudaMemcpyAsync((char *)cx->st + offsetof(PState, K_next), &k0, sizeof k0, cudaMemcpyHostToDevice, s));
+        PCK(cudaStreamSynchronize(s));   // k0 lives on this stack frame
+    }
     PCK(cudaMemsetAsync(cx->dead, 0, kPMaxTile / 8, s));
     PArgs a;
     a.n = (int)r.n; a.ord = r.ordering; a.d = r.d;
     a.N = 1ull << r.n;
     a.tile_min = r.opt.tile_min; a.tile_max = r.opt.tile_max ? r.opt.tile_max : kPDefaultTile;
+    if (a.tile_min > a.tile_max) a.tile_min = a.tile_max;
     a.W0 = r.opt.window0;
     a.growth = (int)r.opt.growth;
+    a.mix = (r.d >= 2 && r.d <= 4 && !(r.opt.flags & GC_FLAG_POPC_ONLY)) ? (int)r.d : 0;
     a.codebook = r.d_codebook; a.capacity = r.capacity;
     a.tabs = cx->tabs; a.vals = cx->vals; a.dead = cx->dead;
     a.q0 = cx->q0; a.q1 = cx->q1; a.surv = cx->surv; a.status = cx->status;

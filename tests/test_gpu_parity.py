@@ -175,10 +175,13 @@ SCHEDULES = [
     {"emulate_ranks": 4, "flags": 1},
     {"flags": 16},                      # host-launched tiles (default 65536)
     {"flags": 16, "tile_max": 4096, "window0": 256},
-    {"tile_max": 8192},                 # beyond the persistent kernel's tiles: launched engine
+    {"tile_max": 8192},
+    {"tile_min": 16384, "tile_max": 16384},   # several resolve chunks per tile
+    {"tile_min": 65536, "tile_max": 65536},
     {"tile_min": 32, "tile_max": 256, "window0": 64},
     {"tile_min": 1024, "tile_max": 1024, "window0": 1 << 14},
     {"window_growth": 1},
+    {"flags": 32},                      # POPC only (no ALU-form checks)
     {"window_growth": 4, "window0": 64},
     {"flags": 16, "window_growth": 3, "window0": 128},
 ]
