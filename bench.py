@@ -33,7 +33,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-POPC_PER_CLK_PER_SM = 16     # measured: profiles/r01_popc_peak.txt (15.35 at the held clock)
+# measured check rates (checks/clk/SM), profiles/r01_popc_peak.txt: the arithmetic the
+# kernel uses for each d (d <= 4: half of the checks in the ALU bit-clearing form)
+CHECK_PEAK_PER_CLK_SM = {"popc": 15.49, 2: 23.62, 3: 19.18, 4: 16.66}
 
 
 def parse_workload(s: str):
@@ -292,7 +294,8 @@ def run_b200(args):
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz") or 1965.0)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = sms * POPC_PER_CLK_PER_SM * sm_max * 1e6
+    per_clk = CHECK_PEAK_PER_CLK_SM.get(d, CHECK_PEAK_PER_CLK_SM["popc"])
+    peak = sms * per_clk * sm_max * 1e6
     achieved = checks / (screen_ms * 1e-3) if screen_ms > 0 else 0.0
     clocks = sampler.summary()
 
@@ -308,11 +311,12 @@ def run_b200(args):
                        "l2": "flushed between timed steps (512 MiB write)"},
             "w_exec": checks / args.steps,
             "w_exec_per_s": (checks / args.steps) / (ms_per_step * 1e-3),
-            "roofline": {"bound": "alu", "kernel": "k_screen (XOR+POPC+IMNMX)",
+            "roofline": {"bound": "alu", "kernel": "k_construct (persistent: screen levels + resolve)",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tchecks/s",
                          "frac": achieved / peak if peak else None, "traffic": load_traffic(),
-                         "peak_basis": f"{sms} SM x {POPC_PER_CLK_PER_SM} POPC/clk/SM x {sm_max:.0f} MHz "
-                                       "(POPC rate measured, profiles/r01_popc_peak.txt)",
+                         "peak_basis": f"{sms} SM x {per_clk} checks/clk/SM x {sm_max:.0f} MHz (check "
+                                       f"arithmetic for d={d} measured by tools/popc_peak.cu, "
+                                       "profiles/r01_popc_peak.txt)",
                          "screen_share_of_step": (screen_ms / args.steps) / ms_per_step,
                          "screen_launches_per_step": stats[-1]["screen_launches"]},
             "e2e": {"value": e2e_val, "unit": "checks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h},

@@ -45,7 +45,9 @@ constexpr uint32_t kPMaxBatches = kPMaxTile / 32;
 constexpr uint32_t kPTargetAccepted = 128;  // adaptive tiles grow up to ~2x this many accepted words
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + s_adjn (1 B) + s_adj (2 B x kPAdj)
-constexpr size_t kPDynSmem = (size_t)kPChunk * (8 + 2 * kPAdj);
+constexpr size_t kPResolveSmem = (size_t)kPChunk * (8 + 2 * kPAdj);
+// + level prefix: s_pre[kPMaxTile/32 + 1] and s_live[kPMaxTile/32]
+constexpr size_t kPDynSmem = kPResolveSmem + (size_t)(2 * (kPMaxTile / 32) + 4) * 4;
 
 struct PState {
     unsigned long long M;
@@ -62,8 +64,6 @@ struct PState {
     unsigned long long n_overflow, n_seq, n_rounds;
     unsigned int error;
     unsigned int K_next;                       // size of the next tile (set by CTA 0)
-    unsigned int q_count[kPMaxLevels + 1];
-    unsigned int bfin[kPMaxLevels][kPMaxBatches];
 };
 
 struct PArgs {
@@ -217,23 +217,36 @@ __device__ __forceinline__ uint32_t p_block_scan(uint32_t x, uint32_t *total, ui
 }
 
 struct PLevel {
-    int l, L;
+    int l;
     uint32_t n_l, B, nsub;
     long long hi, lo, sub;
     unsigned long long t0;
-    const uint2 *qin;
-    uint2 *qout;
+    const uint32_t *s_pre;   // level >= 1: exclusive prefix of live candidates per mask word (smem)
+    const uint32_t *s_live;  // level >= 1: live bits per mask word (smem)
+    uint32_t words;
 };
 
-// One warp item: batch b (32 R candidates) of the level's list against sub-range j of the
-// level's window.  The warp that completes the batch's last sub-range pushes its live
-// candidates to the next level's list.
+// tile index of the q-th live candidate of level >= 1 (q < n_l): the mask word w with
+// s_pre[w] <= q < s_pre[w+1], then the (q - s_pre[w])-th set bit of s_live[w]
+__device__ __forceinline__ uint32_t p_locate(const PLevel &lv, uint32_t q) {
+    uint32_t lo = 0, hi = lv.words;          // s_pre[lo] <= q < s_pre[hi] (s_pre[words] = n_l)
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (lv.s_pre[mid] <= q) lo = mid; else hi = mid;
+    }
+    uint32_t bits = lv.s_live[lo];
+    for (uint32_t k = q - lv.s_pre[lo]; k > 0; --k) bits &= bits - 1;
+    return lo * 32 + (__ffs(bits) - 1);
+}
+
+// One warp item: batch b (32 R candidates) of the level's live candidates against sub-range
+// j of the level's window.  Level 0 generates the candidates from their ranks; deeper levels
+// find them through the CTA's prefix of the dead mask (no lists, no pushes).
 template <int R, int MIX>
 __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigned long long it,
                                        const uint32_t (*C)[33], const uint64_t *off,
                                        unsigned long long &my_checks) {
     const int lane = threadIdx.x & 31;
-    PState *st = a.st;
     const uint32_t j = (uint32_t)(it / lv.B), b = (uint32_t)(it % lv.B);
     const long long s_hi = lv.hi - (long long)j * lv.sub;            // j = 0: newest
     const long long s_lo = max(lv.lo, s_hi - lv.sub);
@@ -243,63 +256,41 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
     bool live[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const uint32_t pos = b * (32u * R) + r * 32 + lane;
-        live[r] = pos < lv.n_l;
+        const uint32_t q = b * (32u * R) + r * 32 + lane;
+        live[r] = q < lv.n_l;
         idx[r] = 0; v[r] = 0;
         if (live[r]) {
-            if (lv.qin) { const uint2 e = __ldcg(lv.qin + pos); idx[r] = e.x; v[r] = e.y; }
-            else {
-                idx[r] = pos;
-                v[r] = rank_to_vector32(a.ord, a.n, C, off, lv.t0 + pos);
-                if (j == 0) a.vals[pos] = v[r];
-                // other sub-ranges of this level may already have killed it
-                if (lv.nsub > 1) live[r] = !((__ldcg(a.dead + (pos >> 5)) >> (pos & 31)) & 1u);
+            if (lv.l == 0) {
+                idx[r] = q;
+                v[r] = rank_to_vector32(a.ord, a.n, C, off, lv.t0 + q);
+                if (j == 0) a.vals[q] = v[r];
+            } else {
+                idx[r] = p_locate(lv, q);
+                v[r] = __ldcg(a.vals + idx[r]);
             }
+            // another sub-range of this level may already have killed it (load issued in
+            // parallel with the value / codeword loads)
+            // (level 0 only: deeper levels hold mostly true survivors, and the load would sit
+            // on their critical path)
+            if (lv.l == 0 && lv.nsub > 1) live[r] = !((__ldcg(a.dead + (idx[r] >> 5)) >> (idx[r] & 31)) & 1u);
         }
         m[r] = live[r] ? 0xffffffffu : 0u;      // dead lanes start "already dead" in both forms
     }
     bool any = false;
 #pragma unroll
     for (int r = 0; r < R; ++r) any |= live[r];
-    bool kill[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) kill[r] = false;
     if (__any_sync(0xffffffffu, any)) {
         const uint32_t sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
         my_checks += (unsigned long long)sc * R;   // per lane; summed over lanes at the end
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            kill[r] = live[r] && p_dead<MIX>(m[r], a.d, r);
-            if (!lv.qin) {
-                const unsigned bb = __ballot_sync(0xffffffffu, kill[r]);
+            const bool kill = live[r] && p_dead<MIX>(m[r], a.d, r);
+            if (lv.l == 0) {
+                // the warp's 32 candidates of this r are one aligned mask word
+                const unsigned bb = __ballot_sync(0xffffffffu, kill);
                 if (lane == 0 && bb) atomicOr(&a.dead[idx[r] >> 5], bb);
-            } else if (kill[r]) {
+            } else if (kill) {
                 atomicOr(&a.dead[idx[r] >> 5], 1u << (idx[r] & 31));
-            }
-        }
-    }
-    if (lv.l + 1 < lv.L) {
-        unsigned last = 1;
-        if (lv.nsub > 1) {
-            __threadfence();
-            if (lane == 0) last = (atomicAdd(&st->bfin[lv.l][b], 1u) + 1u == lv.nsub);
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) __threadfence();
-        }
-        if (last) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const uint32_t pos = b * (32u * R) + r * 32 + lane;
-                bool alive = pos < lv.n_l;
-                if (alive) {
-                    if (lv.nsub > 1) alive = !((__ldcg(a.dead + (idx[r] >> 5)) >> (idx[r] & 31)) & 1u);
-                    else alive = !kill[r];
-                }
-                const unsigned bb = __ballot_sync(0xffffffffu, alive);
-                unsigned base = 0;
-                if (lane == 0 && bb) base = atomicAdd(&st->q_count[lv.l + 1], (unsigned)__popc(bb));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (alive) lv.qout[base + __popc(bb & ((1u << lane) - 1u))] = make_uint2(idx[r], v[r]);
             }
         }
     }
@@ -322,6 +313,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
     uint8_t *s_status = p_dyn + kPChunk * 6;
     uint8_t *s_adjn = p_dyn + kPChunk * 7;
     uint16_t *s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 8);
+    uint32_t *s_pre = reinterpret_cast<uint32_t *>(p_dyn + kPResolveSmem);
+    uint32_t *s_live = s_pre + kPMaxTile / 32 + 4;
     PState *st = a.st;
     const bool graded = a.ord >= GRADED_LEX;
     if (graded) {
@@ -344,17 +337,36 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
         const bool timer = a.timing && blockIdx.x == 0 && threadIdx.x == 0;
         unsigned long long tm = timer ? p_now() : 0, tm_tile = tm;
 
+        const uint32_t words = (K + 31) / 32;
         for (int l = 0; l < L; ++l) {
             // window of level l (newest-first positions), last level reaches 0
             const long long bp = (long long)p_depth(W0, a.growth, l);
             const long long hi = (long long)M - bp;
             long long lo = (l == L - 1) ? 0 : hi - ((long long)W0 << (a.growth * l));
             if (lo < 0) lo = 0;
-            const uint32_t n_l = (l == 0) ? K : __ldcg(&st->q_count[l]);
-            const uint2 *qin = (l == 0) ? nullptr : ((l & 1) ? a.q1 : a.q0);
-            uint2 *qout = (l & 1) ? a.q0 : a.q1;
-            // levels with few live candidates use 32-candidate batches (R = 1) so that partly
-            // filled batches waste fewer lanes; shallow levels use R = 2 (two checks per load)
+            // live candidates of this level: level 0 all K; deeper levels from the dead mask,
+            // compacted through a per-CTA prefix over the mask words (every CTA builds it)
+            uint32_t n_l = K;
+            if (l > 0) {
+                uint32_t tot_all = 0;
+                for (uint32_t w0 = 0; w0 < words; w0 += blockDim.x) {
+                    const uint32_t w = w0 + threadIdx.x;
+                    uint32_t live = 0;
+                    if (w < words) {
+                        live = ~__ldcg(a.dead + w);
+                        if (w * 32 + 32 > K) live &= (1u << (K - w * 32)) - 1u;
+                        s_live[w] = live;
+                    }
+                    uint32_t tot;
+                    const uint32_t pre = tot_all + p_block_scan(__popc(live), &tot, s_ws);
+                    if (w < words) s_pre[w] = pre;
+                    tot_all += tot;
+                }
+                if (threadIdx.x == 0) s_pre[words] = tot_all;
+                __syncthreads();
+                n_l = tot_all;
+            }
+            // levels with few live candidates use 32-candidate batches (R = 1)
             const int R = (n_l >= kPR2Min) ? 2 : 1;
             const uint32_t batch = 32u * R;
             const uint32_t B = (n_l + batch - 1) / batch;
@@ -371,9 +383,9 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                 nsub = (uint32_t)((wlen + sub - 1) / sub);
             }
             PLevel lv;
-            lv.l = l; lv.L = L; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
+            lv.l = l; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
             lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0;
-            lv.qin = qin; lv.qout = qout;
+            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = words;
             const unsigned long long items = (unsigned long long)B * nsub;
             for (unsigned long long it = gwarp; it < items; it += nwarps) {
                 if (R == 2) {
@@ -394,7 +406,6 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
         // ------------------------------------------------ resolve + commit (CTA 0)
         if (blockIdx.x == 0) {
             const uint32_t tid = threadIdx.x;
-            const uint32_t words = (K + 31) / 32;
             if (L == 0) {      // empty codebook: no level generated the candidates
                 for (uint32_t i = tid; i < K; i += blockDim.x) a.vals[i] = rank_to_vector32(a.ord, a.n, C, off, t0 + i);
                 __syncthreads();
@@ -536,9 +547,6 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
             }
             // clear per-tile state for the next tile
             for (uint32_t w = tid; w < words; w += blockDim.x) a.dead[w] = 0;
-            for (int l = 0; l < L; ++l)
-                for (uint32_t b = tid; b < (K + 31) / 32; b += blockDim.x) st->bfin[l][b] = 0;
-            for (int l = tid; l <= kPMaxLevels; l += blockDim.x) st->q_count[l] = 0;
             // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -682,7 +690,7 @@ int persistent_run(const RunArgs &r) {
     if (r.stats) {
         PCK(cudaStreamSynchronize(s));
         PState h;
-        PCK(cudaMemcpy(&h, cx->st, offsetof(PState, q_count), cudaMemcpyDeviceToHost));
+        PCK(cudaMemcpy(&h, cx->st, sizeof(PState), cudaMemcpyDeviceToHost));
         float ms = 0;
         PCK(cudaEventElapsedTime(&ms, cx->ev0, cx->ev1));
         gc_stats *o = r.stats;
@@ -702,7 +710,7 @@ int persistent_run(const RunArgs &r) {
         o->screen_ms = ms;
         if (a.timing) {
             PState full;
-            PCK(cudaMemcpy(&full, cx->st, offsetof(PState, q_count), cudaMemcpyDeviceToHost));
+            PCK(cudaMemcpy(&full, cx->st, sizeof(PState), cudaMemcpyDeviceToHost));
             const double T = (double)full.tiles;
             fprintf(stderr, "[gc] persistent: %llu tiles, per tile: total %.2f us, resolve %.2f us, final sync %.2f us\n",
                     full.tiles, full.t_tile / T / 1e3, full.t_resolve / T / 1e3, full.t_sync / T / 1e3);
