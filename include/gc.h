@@ -88,6 +88,9 @@ typedef struct gc_options {
                                         emulate_ranks paths always use them)                      */
 #define GC_FLAG_POPC_ONLY      0x20u /* every check by XOR+POPC (default for d <= 4: half of them
                                         by an ALU bit-clearing test of the same predicate)         */
+#define GC_FLAG_NO_WEIGHT_BOUND 0x40u /* graded orders: screen the whole codebook (default: stop at the
+                                        first codeword of weight >= wt(candidate) - d + 1, since the
+                                        codebook is weight-sorted and |wt(u)-wt(v)| <= dist(u,v))     */
 #define GC_FLAG_KERNEL_TIMING  0x8u  /* bracket every screen launch with CUDA events on the launching
                                         stream; fills gc_stats.screen_ms (benchmarking)               */
 

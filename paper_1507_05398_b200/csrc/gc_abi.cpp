@@ -51,7 +51,8 @@ int resolve_options(const gc_options *opt, Options *out) {
         return GC_EINVAL;
     }
     if (o.flags & ~(uint32_t)(GC_FLAG_NO_EARLY_EXIT | GC_FLAG_SYNC_TILES | GC_FLAG_FORCE_SEQ_RESOLVE |
-                              GC_FLAG_KERNEL_TIMING | GC_FLAG_LAUNCHED_TILES | GC_FLAG_POPC_ONLY)) {
+                              GC_FLAG_KERNEL_TIMING | GC_FLAG_LAUNCHED_TILES | GC_FLAG_POPC_ONLY |
+                              GC_FLAG_NO_WEIGHT_BOUND)) {
         set_error("unknown bits in gc_options.flags");
         return GC_EINVAL;
     }

@@ -40,14 +40,16 @@ constexpr uint32_t kPSubMin = 64;           // codewords per warp item: at least
 constexpr uint32_t kPSubMax = 2048;         // ... and at most
 constexpr int kPMaxLevels = 32;
 constexpr uint32_t kPMaxTile = 1u << 16;    // largest tile (tile indices fit in 16 bits)
-constexpr uint32_t kPChunk = 1u << 12;      // survivors resolved per chunk (shared memory)
+// survivors resolved per chunk (shared memory): 4096 with one CTA per SM, 2048 with two
 constexpr uint32_t kPMaxBatches = kPMaxTile / 32;
 constexpr uint32_t kPTargetAccepted = 128;  // adaptive tiles grow up to ~2x this many accepted words
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + s_adjn (1 B) + s_adj (2 B x kPAdj)
-constexpr size_t kPResolveSmem = (size_t)kPChunk * (8 + 2 * kPAdj);
+__host__ __device__ constexpr size_t p_resolve_smem(uint32_t chunk) { return (size_t)chunk * (8 + 2 * kPAdj); }
 // + level prefix: s_pre[kPMaxTile/32 + 1] and s_live[kPMaxTile/32]
-constexpr size_t kPDynSmem = kPResolveSmem + (size_t)(2 * (kPMaxTile / 32) + 4) * 4;
+__host__ __device__ constexpr size_t p_dyn_smem(uint32_t chunk) {
+    return p_resolve_smem(chunk) + (size_t)(2 * (kPMaxTile / 32) + 4) * 4;
+}
 
 struct PState {
     unsigned long long M;
@@ -64,6 +66,7 @@ struct PState {
     unsigned long long n_overflow, n_seq, n_rounds;
     unsigned int error;
     unsigned int K_next;                       // size of the next tile (set by CTA 0)
+    unsigned int wfirst[33];                   // graded orders: 1 + index of the first codeword of weight w
 };
 
 struct PArgs {
@@ -73,6 +76,8 @@ struct PArgs {
     uint32_t tile_min, tile_max, W0;
     int growth;
     int mix;                        // 2..4: half the checks via p_clear_low<d> (d <= 4), 0: POPC only
+    uint32_t chunk;                 // survivors per resolve chunk
+    int weight_bound;               // graded orders: stop the screen at the weight bound
     uint32_t *codebook;
     unsigned long long capacity;
     const OrderTables *tabs;
@@ -302,7 +307,9 @@ __device__ __forceinline__ unsigned long long p_now() {
     return t;
 }
 
-__global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
+    const uint32_t kPChunk = a.chunk;
     cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t C[33][33];
     __shared__ uint64_t off[34];
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
     uint8_t *s_status = p_dyn + kPChunk * 6;
     uint8_t *s_adjn = p_dyn + kPChunk * 7;
     uint16_t *s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 8);
-    uint32_t *s_pre = reinterpret_cast<uint32_t *>(p_dyn + kPResolveSmem);
+    uint32_t *s_pre = reinterpret_cast<uint32_t *>(p_dyn + p_resolve_smem(kPChunk));
     uint32_t *s_live = s_pre + kPMaxTile / 32 + 4;
     PState *st = a.st;
     const bool graded = a.ord >= GRADED_LEX;
@@ -332,7 +339,22 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
         const unsigned long long M = __ldcg(&st->M);
         uint32_t K = __ldcg(&st->K_next);
         if ((unsigned long long)K > a.N - t0) K = (uint32_t)(a.N - t0);
-        const int L = p_levels(M, a.W0, a.growth);
+        // Weight bound (graded orders, GC_FLAG_NO_WEIGHT_BOUND unset): the codebook is sorted
+        // by weight and |wt(v) - wt(c)| <= dist(v, c), so codewords of weight < w_lo - (d-1)
+        // (w_lo = weight of the tile's first candidate) are at distance >= d from every
+        // candidate of the tile: the screen stops at the first codeword of weight
+        // >= w_lo - d + 1.  Exact -- only checks whose outcome is known are skipped.
+        unsigned long long base = 0;
+        if (a.weight_bound) {
+            int w_lo = 0;
+            while (t0 >= a.tabs->off[w_lo + 1]) ++w_lo;
+            base = M;
+            for (int w = max(0, w_lo - (int)a.d + 1); w <= a.n; ++w) {
+                const unsigned int f = __ldcg(&st->wfirst[w]);
+                if (f) { base = f - 1; break; }
+            }
+        }
+        const int L = p_levels(M - base, a.W0, a.growth);
         const uint32_t W0 = a.W0;
         const bool timer = a.timing && blockIdx.x == 0 && threadIdx.x == 0;
         unsigned long long tm = timer ? p_now() : 0, tm_tile = tm;
@@ -342,8 +364,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
             // window of level l (newest-first positions), last level reaches 0
             const long long bp = (long long)p_depth(W0, a.growth, l);
             const long long hi = (long long)M - bp;
-            long long lo = (l == L - 1) ? 0 : hi - ((long long)W0 << (a.growth * l));
-            if (lo < 0) lo = 0;
+            long long lo = (l == L - 1) ? (long long)base : hi - ((long long)W0 << (a.growth * l));
+            if (lo < (long long)base) lo = (long long)base;
             // live candidates of this level: level 0 all K; deeper levels from the dead mask,
             // compacted through a per-CTA prefix over the mask words (every CTA builds it)
             uint32_t n_l = K;
@@ -457,9 +479,23 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                     for (uint32_t t = 0; t < A && !prev; ++t)
                         prev = (uint32_t)__popc(vj ^ __ldcg(a.codebook + M0 + t)) < a.d;
                     uint32_t cnt = 0;
-                    for (uint32_t k = 0; k < j; ++k) {
-                        if ((uint32_t)__popc(vj ^ s_val[k]) < a.d) {
-                            if (cnt < kPAdj) s_adj[j * kPAdj + cnt] = (uint16_t)k;
+                    // 32 earlier survivors at a time: independent loads/checks into a bit mask,
+                    // then record the (rare) conflicts
+                    for (uint32_t k0 = 0; k0 < j; k0 += 32) {
+                        const uint32_t kn = min(32u, j - k0);
+                        uint32_t mask = 0;
+                        if (kn == 32) {
+#pragma unroll
+                            for (int t = 0; t < 32; ++t)
+                                mask |= (uint32_t)((uint32_t)__popc(vj ^ s_val[k0 + t]) < a.d) << t;
+                        } else {
+                            for (uint32_t t = 0; t < kn; ++t)
+                                mask |= (uint32_t)((uint32_t)__popc(vj ^ s_val[k0 + t]) < a.d) << t;
+                        }
+                        while (mask) {
+                            const uint32_t t = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            if (cnt < kPAdj) s_adj[j * kPAdj + cnt] = (uint16_t)(k0 + t);
                             ++cnt;
                         }
                     }
@@ -570,6 +606,15 @@ __global__ void __launch_bounds__(kPThreads, 1) k_construct(PArgs a) {
                 unsigned long long M1 = M0 + A;
                 if (M1 > a.capacity) M1 = a.capacity;
                 st->M = M1;
+                if (a.weight_bound) {
+                    // first index of each weight among the words just appended (acceptance
+                    // order is weight-sorted for graded orders); stored +1, 0 = none yet
+                    for (unsigned long long p = M0; p < M1; ++p) {
+                        const uint32_t w = __popc(a.codebook[p]);
+                        if (p == 0 || __popc(a.codebook[p - 1]) != w)
+                            if (!st->wfirst[w]) st->wfirst[w] = (unsigned int)(p + 1);
+                    }
+                }
                 st->K_next = p_next_tile(a, K, S, A, t0 + K, M1);
                 st->survivors += S;
                 st->tiles += 1;
@@ -679,13 +724,20 @@ int persistent_run(const RunArgs &r) {
     a.q0 = cx->q0; a.q1 = cx->q1; a.surv = cx->surv; a.status = cx->status;
     a.st = cx->st; a.d_count = (unsigned long long *)r.d_count;
     a.timing = getenv("GC_DEBUG_PHASES") != nullptr;
+    a.weight_bound = (r.ordering >= GRADED_LEX) && !(r.opt.flags & GC_FLAG_NO_WEIGHT_BOUND);
     int per_sm = 0;
-    PCK(cudaFuncSetAttribute(k_construct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPDynSmem));
-    PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_construct, kPThreads, kPDynSmem));
-    if (per_sm < 1) { set_error("k_construct cannot be resident"); return GC_ECUDA; }
+    // one CTA of 16 warps per SM (128 registers) or two (64 registers, half the resolve chunk)
+    const char *ev = getenv("GC_PERSIST_CTAS");
+    const int ctas = (ev && atoi(ev) == 2) ? 2 : 1;
+    const void *kfn = ctas == 2 ? (const void *)k_construct<2> : (const void *)k_construct<1>;
+    a.chunk = ctas == 2 ? 2048u : 4096u;
+    const size_t smem = p_dyn_smem(a.chunk);
+    PCK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kPThreads, smem));
+    if (per_sm < ctas) { set_error("k_construct cannot be resident"); return GC_ECUDA; }
     void *args[] = {&a};
     PCK(cudaEventRecord(cx->ev0, s));
-    PCK(cudaLaunchCooperativeKernel((const void *)k_construct, dim3(cx->sms), dim3(kPThreads), args, kPDynSmem, s));
+    PCK(cudaLaunchCooperativeKernel(kfn, dim3(cx->sms * ctas), dim3(kPThreads), args, smem, s));
     PCK(cudaEventRecord(cx->ev1, s));
     if (r.stats) {
         PCK(cudaStreamSynchronize(s));

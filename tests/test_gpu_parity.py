@@ -182,6 +182,7 @@ SCHEDULES = [
     {"tile_min": 1024, "tile_max": 1024, "window0": 1 << 14},
     {"window_growth": 1},
     {"flags": 32},                      # POPC only (no ALU-form checks)
+    {"flags": 64},                      # no weight bound (graded orders screen everything)
     {"window_growth": 4, "window0": 64},
     {"flags": 16, "window_growth": 3, "window0": 128},
 ]
