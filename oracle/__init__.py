@@ -70,6 +70,18 @@ def lib():
         L.or_distance.restype = ctypes.c_int
         L.or_weight.argtypes = [ctypes.c_uint32]
         L.or_weight.restype = ctypes.c_int
+        L.or_order_table_basis.argtypes = [ctypes.c_int, u32p, u32p]
+        L.or_order_table_basis.restype = ctypes.c_int
+        L.or_greedy_plain_ex.argtypes = [ctypes.c_int, ctypes.c_int, u32p, ctypes.c_uint64, ctypes.c_int,
+                                         ctypes.c_int, u32p, ctypes.c_uint64]
+        L.or_greedy_plain_ex.restype = ctypes.c_int64
+        L.or_greedy_ball_ex.argtypes = [ctypes.c_int, ctypes.c_int, u32p, ctypes.c_int, ctypes.c_int, u32p,
+                                        ctypes.c_uint64]
+        L.or_greedy_ball_ex.restype = ctypes.c_int64
+        L.or_is_self_orthogonal.argtypes = [u32p, ctypes.c_uint64]
+        L.or_is_self_orthogonal.restype = ctypes.c_int
+        L.or_orthogonal.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
+        L.or_orthogonal.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -208,3 +220,51 @@ def w_def(n: int, ranks_of_accepted) -> int:
     codeword).  = sum_j (2^n - 1 - p_j) over accepted ranks p_j."""
     p = np.asarray(ranks_of_accepted, dtype=np.int64)
     return int(((1 << n) - 1 - p).sum())
+
+
+# ------------------------------------------------ SURVEY 8(f) extension rows
+
+def order_table_basis(n: int, basis) -> np.ndarray:
+    """B-ordering of PAPER.md:119-120 built by its recursive definition."""
+    b = np.ascontiguousarray(np.asarray(basis, dtype=np.uint32))
+    if len(b) != n:
+        raise ValueError("basis must have n vectors")
+    t = np.empty(1 << n, dtype=np.uint32)
+    if lib().or_order_table_basis(n, _p(b), _p(t)) != 0:
+        raise ValueError("basis is not linearly independent over F_2 (or out of range)")
+    return t
+
+
+def orthogonal(u: int, v: int) -> bool:
+    return bool(lib().or_orthogonal(u, v))
+
+
+def is_self_orthogonal(words) -> bool:
+    w = np.ascontiguousarray(np.asarray(words, dtype=np.uint32))
+    return bool(lib().or_is_self_orthogonal(_p(w), len(w)))
+
+
+def greedy_plain_ex(n, d, ordering="lex", constant_weight=-1, self_orthogonal=False, table=None, basis=None):
+    """O1 with the constant-weight / self-orthogonal (:122-123) constraints,
+    over any ordering (a name, a B-ordering basis, or a table)."""
+    if table is None:
+        table = order_table_basis(n, basis) if basis is not None else order_table(ordering, n)
+    cap = min(1 << n, hamming_bound(n, d))
+    out = np.empty(max(cap, 1), dtype=np.uint32)
+    M = lib().or_greedy_plain_ex(n, d, _p(table), 1 << n, int(constant_weight), int(bool(self_orthogonal)),
+                                 _p(out), cap)
+    if M < 0:
+        raise RuntimeError(f"or_greedy_plain_ex -> {M}")
+    return out[:M].copy()
+
+
+def greedy_ball_ex(n, d, ordering="lex", constant_weight=-1, self_orthogonal=False, table=None, basis=None):
+    """O2 with the same constraints (ball map for distance, span basis for orthogonality)."""
+    if table is None:
+        table = order_table_basis(n, basis) if basis is not None else order_table(ordering, n)
+    cap = min(1 << n, hamming_bound(n, d))
+    out = np.empty(max(cap, 1), dtype=np.uint32)
+    M = lib().or_greedy_ball_ex(n, d, _p(table), int(constant_weight), int(bool(self_orthogonal)), _p(out), cap)
+    if M < 0:
+        raise RuntimeError(f"or_greedy_ball_ex -> {M}")
+    return out[:M].copy()
