@@ -142,6 +142,36 @@ int gc_generate_device(uint32_t n, uint32_t d, gc_ordering ordering, const gc_op
                        uint32_t *d_codebook, uint64_t capacity, uint64_t *d_count,
                        void *stream, gc_stats *stats);
 
+/* ------------------------------------------------ generalised problem */
+
+/* The constructions of PAPER.md Sec. 3-4 beyond the base greedy:
+ *   - B-ordering: ordering = GC_B_ORDERING and basis = n linearly
+ *     independent vectors b_1..b_n (HOST memory, caller-owned, read during the call);
+ *     rank r -> XOR of b_{j+1} over the set bits j of r, i.e. {0, b_1, b_2, b_2+b_1, ...};
+ *   - self-orthogonal greedy codes: a candidate must also be orthogonal
+ *     to itself (even weight) and to every accepted word (popcount(v & c) even);
+ *   - constant-weight codes: only candidates of weight constant_weight.
+ * The ordering still defines the scan; filtered candidates are never accepted.  Supported
+ * by the single-GPU persistent engine (GC_EUNSUPPORTED with emulate_ranks > 1 or
+ * GC_FLAG_LAUNCHED_TILES / NO_EARLY_EXIT / FORCE_SEQ_RESOLVE).  gc_stats.w_def is 0 for
+ * filtered problems (its definition counts every rank). */
+#define GC_B_ORDERING 4
+typedef struct gc_problem {
+    uint32_t struct_size;        /* sizeof(gc_problem)                                        */
+    uint32_t n, d;               /* 1 <= d <= n <= 32                                         */
+    int32_t ordering;            /* gc_ordering value, or GC_B_ORDERING                        */
+    const uint64_t *basis;       /* GC_B_ORDERING: n vectors < 2^n, independent over F_2       */
+    int32_t constant_weight;     /* -1: no constraint, else 0..n                               */
+    uint32_t self_orthogonal;    /* 0 or 1                                                     */
+} gc_problem;
+
+/* As gc_generate_ex / gc_generate_device for a gc_problem.  GC_EINVAL for a dependent or
+ * out-of-range basis, a bad weight or flag. */
+int gc_construct(const gc_problem *problem, const gc_options *opt, uint64_t *out_codewords,
+                 uint64_t *out_count, gc_stats *stats);
+int gc_construct_device(const gc_problem *problem, const gc_options *opt, uint32_t *d_codebook,
+                        uint64_t capacity, uint64_t *d_count, void *stream, gc_stats *stats);
+
 /* Upper bound on M: the sphere-packing (Hamming) bound for (n, d); for even d the
  * bound of (n-1, d-1) (a code of even distance d and length n punctures to one of
  * length n-1 and distance d-1).  Clamped to 2^n.  Returns 0 if the arguments are invalid.

@@ -18,6 +18,7 @@ from ._binding import (  # noqa: F401
     GC_FLAG_NO_WEIGHT_BOUND,
     GC_FLAG_POPC_ONLY,
     GC_FLAG_SYNC_TILES,
+    GC_B_ORDERING,
     GC_GRADED_LEX,
     GC_GRADED_REVLEX,
     GC_GRAY,
@@ -31,6 +32,8 @@ from ._binding import (  # noqa: F401
     gc_capacity_bound,
     gc_comm_create,
     gc_comm_destroy,
+    gc_construct,
+    gc_construct_device,
     gc_generate,
     gc_generate_device,
     gc_generate_ex,

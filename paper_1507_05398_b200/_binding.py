@@ -38,6 +38,15 @@ class gc_options(ctypes.Structure):
                 ("window_growth", ctypes.c_uint32)]
 
 
+GC_B_ORDERING = 4
+
+
+class gc_problem(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("n", ctypes.c_uint32), ("d", ctypes.c_uint32),
+                ("ordering", ctypes.c_int32), ("basis", ctypes.POINTER(ctypes.c_uint64)),
+                ("constant_weight", ctypes.c_int32), ("self_orthogonal", ctypes.c_uint32)]
+
+
 class gc_stats(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("n_ranks", ctypes.c_uint32),
                 ("device_ms", ctypes.c_double), ("wall_ms", ctypes.c_double),
@@ -70,6 +79,11 @@ _sig("gc_generate_device", ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, ctyp
                                           ctypes.POINTER(gc_options), ctypes.c_void_p, ctypes.c_uint64,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(gc_stats)])
 _sig("gc_capacity_bound", ctypes.c_uint64, [ctypes.c_uint32, ctypes.c_uint32])
+_sig("gc_construct", ctypes.c_int, [ctypes.POINTER(gc_problem), ctypes.POINTER(gc_options), _u64p, _u64p,
+                                    ctypes.POINTER(gc_stats)])
+_sig("gc_construct_device", ctypes.c_int, [ctypes.POINTER(gc_problem), ctypes.POINTER(gc_options),
+                                           ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.POINTER(gc_stats)])
 _sig("gc_rank_to_vector", ctypes.c_int, [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64, _u64p])
 _sig("gc_vector_to_rank", ctypes.c_int, [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64, _u64p])
 _sig("gc_ranks_to_vectors", ctypes.c_int, [ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, _u64p])
@@ -187,6 +201,54 @@ def gc_generate_device(n: int, d: int, ordering, codebook, count, stream=None, o
     cap = codebook.numel() * codebook.element_size() // 4
     _check(_lib.gc_generate_device(n, d, ordering_id(ordering), _ref(o), codebook.data_ptr(), cap,
                                    count.data_ptr(), _stream_ptr(stream), _ref(st)), "gc_generate_device")
+    return st.to_dict() if st is not None else None
+
+
+def _problem(n, d, ordering="lex", basis=None, constant_weight=-1, self_orthogonal=False):
+    p = gc_problem()
+    p.struct_size = ctypes.sizeof(gc_problem)
+    p.n, p.d = n, d
+    keep = None
+    if basis is not None:
+        keep = (ctypes.c_uint64 * len(basis))(*[int(x) for x in basis])
+        p.basis = ctypes.cast(keep, ctypes.POINTER(ctypes.c_uint64))
+        p.ordering = GC_B_ORDERING
+    else:
+        p.ordering = ordering_id(ordering)
+    p.constant_weight = int(constant_weight)
+    p.self_orthogonal = int(bool(self_orthogonal))
+    return p, keep
+
+
+def gc_construct(n: int, d: int, ordering="lex", basis=None, constant_weight=-1, self_orthogonal=False,
+                 options=None, capacity: int | None = None):
+    """Generalised construction (B-ordering basis, constant weight, self-orthogonal) --
+    gc_construct().  Returns (codewords uint64 array, stats dict)."""
+    prob, keep = _problem(n, d, ordering, basis, constant_weight, self_orthogonal)
+    cap = gc_capacity_bound(n, d) if capacity is None else capacity
+    out = np.zeros(max(cap, 1), dtype=np.uint64)
+    cnt = ctypes.c_uint64(cap)
+    st = gc_stats()
+    st.struct_size = ctypes.sizeof(gc_stats)
+    o = _opts(options)
+    _check(_lib.gc_construct(ctypes.byref(prob), _ref(o), out.ctypes.data_as(_u64p), ctypes.byref(cnt),
+                             ctypes.byref(st)), "gc_construct")
+    del keep
+    return out[: cnt.value], st.to_dict()
+
+
+def gc_construct_device(n: int, d: int, codebook, count, ordering="lex", basis=None, constant_weight=-1,
+                        self_orthogonal=False, stream=None, options=None, stats: bool = False):
+    prob, keep = _problem(n, d, ordering, basis, constant_weight, self_orthogonal)
+    o = _opts(options)
+    st = None
+    if stats:
+        st = gc_stats()
+        st.struct_size = ctypes.sizeof(gc_stats)
+    cap = codebook.numel() * codebook.element_size() // 4
+    _check(_lib.gc_construct_device(ctypes.byref(prob), _ref(o), codebook.data_ptr(), cap, count.data_ptr(),
+                                    _stream_ptr(stream), _ref(st)), "gc_construct_device")
+    del keep
     return st.to_dict() if st is not None else None
 
 

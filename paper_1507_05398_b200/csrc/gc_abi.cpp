@@ -163,6 +163,43 @@ void nccl_comm_destroy(void *comm) {
     if (comm && nccl_api()) nccl_api()->CommDestroy(comm);
 }
 
+// validate a gc_problem into RunArgs (before any CUDA call)
+int gc_problem_to_args(const gc_problem *p, RunArgs *a) {
+    if (!p) { set_error("problem is NULL"); return GC_EINVAL; }
+    if (p->struct_size != 0 && p->struct_size < sizeof(gc_problem)) { set_error("gc_problem.struct_size too small"); return GC_EINVAL; }
+    const int ord = p->ordering;
+    if (ord < GC_LEX || ord > GC_B_ORDERING) { set_error("unknown ordering"); return GC_EINVAL; }
+    if (p->n == 0) { set_error("n must be >= 1"); return GC_EINVAL; }
+    if (p->d == 0 || p->d > p->n) { set_error("d must be in [1, n]"); return GC_EINVAL; }
+    if (p->n > 32) { set_error("the GPU path supports n <= 32"); return GC_EUNSUPPORTED; }
+    if (p->constant_weight < -1 || p->constant_weight > (int)p->n) { set_error("constant_weight must be -1 or in [0, n]"); return GC_EINVAL; }
+    if (p->self_orthogonal > 1) { set_error("self_orthogonal must be 0 or 1"); return GC_EINVAL; }
+    a->n = p->n; a->d = p->d;
+    a->ordering = ord == GC_B_ORDERING ? GC_LEX : ord;
+    a->constant_weight = p->constant_weight;
+    a->self_orthogonal = p->self_orthogonal != 0;
+    if (ord == GC_B_ORDERING) {
+        if (!p->basis) { set_error("GC_B_ORDERING needs a basis"); return GC_EINVAL; }
+        uint64_t red[64] = {0};
+        for (uint32_t k = 0; k < p->n; ++k) {
+            uint64_t x = p->basis[k];
+            if (x >> p->n) { set_error("basis vector >= 2^n"); return GC_EINVAL; }
+            for (int b = 63; b >= 0 && x; --b) {
+                if (!(x >> b & 1ull)) continue;
+                if (!red[b]) { red[b] = x; x = 0; break; }
+                x ^= red[b];
+            }
+
+            a->basis[k] = (uint32_t)p->basis[k];
+        }
+        int rank = 0;
+        for (int b = 0; b < 64; ++b) rank += red[b] != 0;
+        if (rank != (int)p->n) { set_error("basis is not linearly independent over F_2"); return GC_EINVAL; }
+        a->use_basis = true;
+    }
+    return GC_OK;
+}
+
 }  // namespace gc
 
 using namespace gc;
@@ -298,6 +335,24 @@ int gc_generate_device(uint32_t n, uint32_t d, gc_ordering ordering, const gc_op
 
 int gc_generate_ex(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt,
                    uint64_t *out_codewords, uint64_t *out_count, gc_stats *stats);
+
+int gc_construct_device(const gc_problem *problem, const gc_options *opt, uint32_t *d_codebook, uint64_t capacity,
+                        uint64_t *d_count, void *stream, gc_stats *stats) {
+    clear_error();
+    RunArgs a;
+    int rc = gc_problem_to_args(problem, &a);
+    if (rc) return rc;
+    rc = resolve_options(opt, &a.opt);
+    if (rc) return rc;
+    if (!d_codebook || !d_count || capacity == 0) { set_error("d_codebook/d_count NULL or capacity 0"); return GC_EINVAL; }
+    if (stats && stats->struct_size != 0 && stats->struct_size < sizeof(gc_stats)) {
+        set_error("gc_stats.struct_size too small");
+        return GC_EINVAL;
+    }
+    a.d_codebook = d_codebook; a.capacity = capacity; a.d_count = d_count;
+    a.stream = stream; a.stats = stats;
+    return engine_run(a);
+}
 
 int gc_generate(uint32_t n, uint32_t d, gc_ordering ordering, uint64_t *out_codewords, uint64_t *out_count) {
     return gc_generate_ex(n, d, ordering, nullptr, out_codewords, out_count, nullptr);

@@ -522,6 +522,11 @@ static int phases_for(unsigned long long M_ub, uint32_t W0, uint32_t growth) {
 
 int engine_run(const RunArgs &a) {
     auto wall0 = std::chrono::steady_clock::now();
+    if (a.extended() && !persistent_supported(a)) {
+        set_error("B-ordering / self-orthogonal / constant-weight problems run on the single-GPU persistent "
+                  "engine only (no emulate_ranks, launched tiles, no-early-exit or sequential-resolve flags)");
+        return GC_EUNSUPPORTED;
+    }
     if (persistent_supported(a)) {
         int rc = persistent_run(a);
         if (a.stats) a.stats->wall_ms =
@@ -705,6 +710,24 @@ int engine_ranks_to_vectors_device(int ordering, uint32_t n, uint64_t first, uin
 
 using namespace gc;
 
+// host-buffer construction shared by gc_generate_ex and gc_construct (args validated)
+static int host_construct(RunArgs &a, uint64_t *out_codewords, uint64_t *out_count, gc_stats *stats);
+
+extern "C" int gc_construct(const gc_problem *problem, const gc_options *opt, uint64_t *out_codewords,
+                            uint64_t *out_count, gc_stats *stats) {
+    clear_error();
+    if (!out_count) { set_error("out_count is NULL"); return GC_EINVAL; }
+    if (!out_codewords && *out_count) { set_error("out_codewords is NULL with capacity > 0"); return GC_EINVAL; }
+    gc_problem base{};
+    RunArgs a;
+    int rc = gc_problem_to_args(problem, &a);
+    (void)base;
+    if (rc) return rc;
+    rc = resolve_options(opt, &a.opt);
+    if (rc) return rc;
+    return host_construct(a, out_codewords, out_count, stats);
+}
+
 extern "C" int gc_generate_ex(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt,
                               uint64_t *out_codewords, uint64_t *out_count, gc_stats *stats) {
     clear_error();
@@ -717,6 +740,13 @@ extern "C" int gc_generate_ex(uint32_t n, uint32_t d, gc_ordering ordering, cons
     RunArgs a;
     int rc = resolve_options(opt, &a.opt);
     if (rc) return rc;
+    a.n = n; a.d = d; a.ordering = ordering;
+    return host_construct(a, out_codewords, out_count, stats);
+}
+
+static int host_construct(RunArgs &a, uint64_t *out_codewords, uint64_t *out_count, gc_stats *stats) {
+    int rc;
+    const uint32_t n = a.n, d = a.d;
     const uint64_t cap = gc_capacity_bound(n, d);
     uint32_t *d_cb = nullptr;
     unsigned long long *d_cnt = nullptr;
@@ -727,7 +757,6 @@ extern "C" int gc_generate_ex(uint32_t n, uint32_t d, gc_ordering ordering, cons
         return GC_ENOMEM;
     }
     gc_stats local{};
-    a.n = n; a.d = d; a.ordering = ordering;
     a.d_codebook = d_cb; a.capacity = cap; a.d_count = (uint64_t *)d_cnt;
     a.stream = nullptr; a.stats = stats ? stats : &local;
     rc = engine_run(a);

@@ -54,8 +54,15 @@ struct RunArgs {
     uint64_t *d_count = nullptr;    // device
     void *stream = nullptr;
     gc_stats *stats = nullptr;      // non-null -> synchronise and fill
+    // SURVEY 8(f) extensions (persistent engine only)
+    bool use_basis = false;
+    uint32_t basis[32] = {0};
+    bool self_orthogonal = false;
+    int constant_weight = -1;
+    bool extended() const { return use_basis || self_orthogonal || constant_weight >= 0; }
 };
 int engine_run(const RunArgs &a);
+int gc_problem_to_args(const gc_problem *p, RunArgs *a);   // gc_abi.cpp (validation, no CUDA)
 bool persistent_supported(const RunArgs &a);   // gc_persistent.cu
 int persistent_run(const RunArgs &a);
 int engine_ranks_to_vectors_device(int ordering, uint32_t n, uint64_t first, uint64_t count,

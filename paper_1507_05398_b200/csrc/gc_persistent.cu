@@ -78,6 +78,13 @@ struct PArgs {
     int mix;                        // 2..4: half the checks via p_clear_low<d> (d <= 4), 0: POPC only
     uint32_t chunk;                 // survivors per resolve chunk
     int weight_bound;               // graded orders: stop the screen at the weight bound
+    // SURVEY 8(f) extensions
+    int use_basis;                  // B-ordering: rank -> XOR of basis[j] over set bits j
+    uint32_t basis[32];
+    int so;                         // self-orthogonal: also popc(v & c) even, wt(v) even
+    int cw;                         // constant weight (-1: none)
+    unsigned long long t_begin, t_end;   // ranks scanned (graded + constant weight: one class)
+    int wdef_valid;                 // W_def counts every rank: only without filters
     uint32_t *codebook;
     unsigned long long capacity;
     const OrderTables *tabs;
@@ -142,13 +149,19 @@ __device__ __forceinline__ uint32_t p_clear_low(uint32_t x) {
 // the two halves of a warp's checks use different pipes.
 template <int MIX>
 __device__ __forceinline__ void p_check(uint32_t &m, uint32_t v, uint32_t c, int r) {
-    if (MIX && (r & 1)) m = min(m, p_clear_low<MIX>(v ^ c));
-    else m = min(m, (uint32_t)__popc(v ^ c));
+    if (MIX == 1) {
+        // self-orthogonal: odd AND-parity counts as a violation (distance 0)
+        m = min(m, (__popc(v & c) & 1) ? 0u : (uint32_t)__popc(v ^ c));
+    } else if (MIX && (r & 1)) {
+        m = min(m, p_clear_low<MIX>(v ^ c));
+    } else {
+        m = min(m, (uint32_t)__popc(v ^ c));
+    }
 }
 
 template <int MIX>
 __device__ __forceinline__ bool p_dead(uint32_t m, uint32_t d, int r) {
-    return (MIX && (r & 1)) ? (m == 0) : (m < d);
+    return (MIX >= 2 && (r & 1)) ? (m == 0) : (m < d);
 }
 
 // scan codewords [a, b) newest first for the lane's R candidates; returns the number of
@@ -221,6 +234,28 @@ __device__ __forceinline__ uint32_t p_block_scan(uint32_t x, uint32_t *total, ui
     return r;
 }
 
+// u and v cannot both be in the code: distance < d, or (self-orthogonal) odd AND-parity
+__device__ __forceinline__ bool p_conflict(const PArgs &a, uint32_t u, uint32_t v) {
+    return (uint32_t)__popc(u ^ v) < a.d || (a.so && (__popc(u & v) & 1));
+}
+
+// candidate of rank r: the ordering's vector, or the B-ordering's XOR of basis vectors
+__device__ __forceinline__ uint32_t p_gen(const PArgs &a, const uint32_t (*C)[33], const uint64_t *off,
+                                          const uint32_t *basis, unsigned long long r) {
+    if (a.use_basis) {
+        uint32_t v = 0;
+        for (uint32_t bits = (uint32_t)r; bits; bits &= bits - 1) v ^= basis[__ffs(bits) - 1];
+        return v;
+    }
+    return rank_to_vector32(a.ord, a.n, C, off, r);
+}
+
+// candidate considered at all: constant weight, even weight if self-orthogonal
+__device__ __forceinline__ bool p_allowed(const PArgs &a, uint32_t v) {
+    const int w = __popc(v);
+    return (a.cw < 0 || w == a.cw) && (!a.so || !(w & 1));
+}
+
 struct PLevel {
     int l;
     uint32_t n_l, B, nsub;
@@ -229,6 +264,7 @@ struct PLevel {
     const uint32_t *s_pre;   // level >= 1: exclusive prefix of live candidates per mask word (smem)
     const uint32_t *s_live;  // level >= 1: live bits per mask word (smem)
     uint32_t words;
+    const uint32_t *basis;   // B-ordering basis (smem)
 };
 
 // tile index of the q-th live candidate of level >= 1 (q < n_l): the mask word w with
@@ -258,17 +294,19 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
     // first codeword block in flight while the candidates are fetched
     const uint32_t cur0 = (s_hi - 1 - lane >= s_lo) ? __ldcg(a.codebook + s_hi - 1 - lane) : 0u;
     uint32_t v[R], m[R], idx[R];
-    bool live[R];
+    bool live[R], filtered[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t q = b * (32u * R) + r * 32 + lane;
         live[r] = q < lv.n_l;
+        filtered[r] = false;
         idx[r] = 0; v[r] = 0;
         if (live[r]) {
             if (lv.l == 0) {
                 idx[r] = q;
-                v[r] = rank_to_vector32(a.ord, a.n, C, off, lv.t0 + q);
+                v[r] = p_gen(a, C, off, lv.basis, lv.t0 + q);
                 if (j == 0) a.vals[q] = v[r];
+                if (!p_allowed(a, v[r])) { filtered[r] = true; live[r] = false; }
             } else {
                 idx[r] = p_locate(lv, q);
                 v[r] = __ldcg(a.vals + idx[r]);
@@ -277,19 +315,26 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
             // parallel with the value / codeword loads)
             // (level 0 only: deeper levels hold mostly true survivors, and the load would sit
             // on their critical path)
-            if (lv.l == 0 && lv.nsub > 1) live[r] = !((__ldcg(a.dead + (idx[r] >> 5)) >> (idx[r] & 31)) & 1u);
+            if (lv.l == 0 && lv.nsub > 1 && live[r])
+                live[r] = !((__ldcg(a.dead + (idx[r] >> 5)) >> (idx[r] & 31)) & 1u);
         }
         m[r] = live[r] ? 0xffffffffu : 0u;      // dead lanes start "already dead" in both forms
     }
     bool any = false;
 #pragma unroll
     for (int r = 0; r < R; ++r) any |= live[r];
-    if (__any_sync(0xffffffffu, any)) {
-        const uint32_t sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
-        my_checks += (unsigned long long)sc * R;   // per lane; summed over lanes at the end
+    bool any_filtered = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) any_filtered |= filtered[r];
+    const bool scan = __any_sync(0xffffffffu, any);
+    if (scan || __any_sync(0xffffffffu, any_filtered)) {
+        if (scan) {
+            const uint32_t sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
+            my_checks += (unsigned long long)sc * R;   // per lane; summed over lanes at the end
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const bool kill = live[r] && p_dead<MIX>(m[r], a.d, r);
+            const bool kill = filtered[r] || (live[r] && p_dead<MIX>(m[r], a.d, r));
             if (lv.l == 0) {
                 // the warp's 32 candidates of this r are one aligned mask word
                 const unsigned bb = __ballot_sync(0xffffffffu, kill);
@@ -322,7 +367,9 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     uint16_t *s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 8);
     uint32_t *s_pre = reinterpret_cast<uint32_t *>(p_dyn + p_resolve_smem(kPChunk));
     uint32_t *s_live = s_pre + kPMaxTile / 32 + 4;
+    __shared__ uint32_t s_basis[32];
     PState *st = a.st;
+    if (threadIdx.x < 32) s_basis[threadIdx.x] = a.basis[threadIdx.x];
     const bool graded = a.ord >= GRADED_LEX;
     if (graded) {
         for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) C[i / 33][i % 33] = a.tabs->binom[i / 33][i % 33];
@@ -334,11 +381,11 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     const uint32_t nwarps = gridDim.x * kPWarps;
     unsigned long long my_checks = 0;
 
-    unsigned long long t0 = 0;
-    while (t0 < a.N) {
+    unsigned long long t0 = a.t_begin;
+    while (t0 < a.t_end) {
         const unsigned long long M = __ldcg(&st->M);
         uint32_t K = __ldcg(&st->K_next);
-        if ((unsigned long long)K > a.N - t0) K = (uint32_t)(a.N - t0);
+        if ((unsigned long long)K > a.t_end - t0) K = (uint32_t)(a.t_end - t0);
         // Weight bound (graded orders, GC_FLAG_NO_WEIGHT_BOUND unset): the codebook is sorted
         // by weight and |wt(v) - wt(c)| <= dist(v, c), so codewords of weight < w_lo - (d-1)
         // (w_lo = weight of the tile's first candidate) are at distance >= d from every
@@ -407,10 +454,13 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             PLevel lv;
             lv.l = l; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
             lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0;
-            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = words;
+            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = words; lv.basis = s_basis;
             const unsigned long long items = (unsigned long long)B * nsub;
             for (unsigned long long it = gwarp; it < items; it += nwarps) {
-                if (R == 2) {
+                if (a.so) {
+                    if (R == 2) p_item<2, 1>(a, lv, it, C, off, my_checks);
+                    else p_item<1, 1>(a, lv, it, C, off, my_checks);
+                } else if (R == 2) {
                     switch (a.mix) {
                         case 2: p_item<2, 2>(a, lv, it, C, off, my_checks); break;
                         case 3: p_item<2, 3>(a, lv, it, C, off, my_checks); break;
@@ -429,7 +479,11 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
         if (blockIdx.x == 0) {
             const uint32_t tid = threadIdx.x;
             if (L == 0) {      // empty codebook: no level generated the candidates
-                for (uint32_t i = tid; i < K; i += blockDim.x) a.vals[i] = rank_to_vector32(a.ord, a.n, C, off, t0 + i);
+                for (uint32_t i = tid; i < K; i += blockDim.x) {
+                    const uint32_t v = p_gen(a, C, off, s_basis, t0 + i);
+                    a.vals[i] = v;
+                    if (!p_allowed(a, v)) atomicOr(&a.dead[i >> 5], 1u << (i & 31));
+                }
                 __syncthreads();
             }
             // survivors in rank order -> a.surv (global; S <= K)
@@ -477,7 +531,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                     const uint32_t vj = s_val[j];
                     bool prev = false;
                     for (uint32_t t = 0; t < A && !prev; ++t)
-                        prev = (uint32_t)__popc(vj ^ __ldcg(a.codebook + M0 + t)) < a.d;
+                        prev = p_conflict(a, vj, __ldcg(a.codebook + M0 + t));
                     uint32_t cnt = 0;
                     // 32 earlier survivors at a time: independent loads/checks into a bit mask,
                     // then record the (rare) conflicts
@@ -487,10 +541,10 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                         if (kn == 32) {
 #pragma unroll
                             for (int t = 0; t < 32; ++t)
-                                mask |= (uint32_t)((uint32_t)__popc(vj ^ s_val[k0 + t]) < a.d) << t;
+                                mask |= (uint32_t)p_conflict(a, vj, s_val[k0 + t]) << t;
                         } else {
                             for (uint32_t t = 0; t < kn; ++t)
-                                mask |= (uint32_t)((uint32_t)__popc(vj ^ s_val[k0 + t]) < a.d) << t;
+                                mask |= (uint32_t)p_conflict(a, vj, s_val[k0 + t]) << t;
                         }
                         while (mask) {
                             const uint32_t t = __ffs(mask) - 1;
@@ -527,7 +581,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                         } else {
                             const uint32_t vj = s_val[j];
                             for (uint32_t k = 0; k < j; ++k) {
-                                if ((uint32_t)__popc(vj ^ s_val[k]) < a.d) {
+                                if (p_conflict(a, vj, s_val[k])) {
                                     const uint8_t sk = s_status[k];
                                     acc_nb |= sk == 1;
                                     und_nb |= sk == 2;
@@ -554,7 +608,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                         } else {
                             const uint32_t vj = s_val[j];
                             for (uint32_t k = lane; k < j; k += 32)
-                                acc_nb |= (s_status[k] == 1) && (uint32_t)__popc(vj ^ s_val[k]) < a.d;
+                                acc_nb |= (s_status[k] == 1) && p_conflict(a, vj, s_val[k]);
                         }
                         acc_nb = __any_sync(0xffffffffu, acc_nb);
                         if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
@@ -572,7 +626,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                     if (acc) {
                         if (M0 + pos < a.capacity) a.codebook[M0 + pos] = s_val[j];
                         else st->error = 1;
-                        wdef += a.N - 1 - (t0 + s_idx[j]);
+                        if (a.wdef_valid) wdef += a.N - 1 - (t0 + s_idx[j]);
                     }
                     A += tot;
                 }
@@ -724,7 +778,23 @@ int persistent_run(const RunArgs &r) {
     a.q0 = cx->q0; a.q1 = cx->q1; a.surv = cx->surv; a.status = cx->status;
     a.st = cx->st; a.d_count = (unsigned long long *)r.d_count;
     a.timing = getenv("GC_DEBUG_PHASES") != nullptr;
-    a.weight_bound = (r.ordering >= GRADED_LEX) && !(r.opt.flags & GC_FLAG_NO_WEIGHT_BOUND);
+    a.use_basis = r.use_basis;
+    for (int i = 0; i < 32; ++i) a.basis[i] = r.basis[i];
+    a.so = r.self_orthogonal;
+    a.cw = r.constant_weight;
+    a.wdef_valid = !(r.self_orthogonal || r.constant_weight >= 0);
+    // the weight bound is a distance argument: not valid for the orthogonality constraint
+    a.weight_bound = (r.ordering >= GRADED_LEX) && !r.use_basis && !r.self_orthogonal &&
+                     !(r.opt.flags & GC_FLAG_NO_WEIGHT_BOUND);
+    a.t_begin = 0;
+    a.t_end = a.N;
+    if (r.constant_weight >= 0 && r.ordering >= GRADED_LEX && !r.use_basis) {
+        OrderTables t;
+        build_order_tables((int)r.n, &t);
+        a.t_begin = t.off[r.constant_weight];        // graded orders: the weight class is one
+        a.t_end = t.off[r.constant_weight + 1];      // contiguous block of ranks
+    }
+    if (a.mix && r.self_orthogonal) a.mix = 0;
     int per_sm = 0;
     // one CTA of 16 warps per SM (128 registers) or two (64 registers, half the resolve chunk)
     const char *ev = getenv("GC_PERSIST_CTAS");

@@ -146,3 +146,24 @@ def test_host_ordering_errors():
     with pytest.raises(gc.GCError) as e:
         gc.gc_rank_to_vector("lex", 64, 1)
     assert e.value.name == "GC_EINVAL"
+
+
+def test_construct_validates_problem():
+    for kw, status in [
+        (dict(n=5, d=2, basis=[1, 2, 3, 8, 16]), "GC_EINVAL"),          # dependent basis
+        (dict(n=5, d=2, basis=[1, 2, 4, 8, 32]), "GC_EINVAL"),          # vector >= 2^n
+        (dict(n=5, d=2, basis=[1, 2, 4, 8, 0]), "GC_EINVAL"),           # zero vector
+        (dict(n=5, d=2, constant_weight=6), "GC_EINVAL"),
+        (dict(n=5, d=2, constant_weight=-2), "GC_EINVAL"),
+        (dict(n=5, d=6), "GC_EINVAL"),
+        (dict(n=33, d=3), "GC_EUNSUPPORTED"),
+    ]:
+        with pytest.raises(gc.GCError) as e:
+            gc.gc_construct(**kw, capacity=64)
+        assert e.value.name == status, kw
+    # emulate_ranks cannot carry the extensions
+    import torch
+    if not torch.cuda.is_available():
+        with pytest.raises(gc.GCError) as e:
+            gc.gc_construct(8, 3, self_orthogonal=True, options={"emulate_ranks": 2}, capacity=64)
+        assert e.value.name in ("GC_EUNSUPPORTED", "GC_ECUDA")
