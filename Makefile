@@ -19,7 +19,10 @@ $(SRC)/gc_abi.o: $(SRC)/gc_abi.cpp $(SRC)/gc_internal.h include/gc.h
 $(SRC)/gc_persistent.o: $(SRC)/gc_persistent.cu $(SRC)/gc_order.cuh $(SRC)/gc_internal.h include/gc.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_persistent.ptxas.log || (cat $(SRC)/gc_persistent.ptxas.log; false)
 
-$(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o $(SRC)/gc_persistent.o
+$(SRC)/gc_analysis.o: $(SRC)/gc_analysis.cu $(SRC)/gc_internal.h include/gc.h
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_analysis.ptxas.log || (cat $(SRC)/gc_analysis.ptxas.log; false)
+
+$(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o $(SRC)/gc_persistent.o $(SRC)/gc_analysis.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
 
 $(ORACLE): oracle/greedy_oracle.c

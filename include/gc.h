@@ -172,6 +172,37 @@ int gc_construct(const gc_problem *problem, const gc_options *opt, uint64_t *out
 int gc_construct_device(const gc_problem *problem, const gc_options *opt, uint32_t *d_codebook,
                         uint64_t capacity, uint64_t *d_count, void *stream, gc_stats *stats);
 
+/* ------------------------------------------------ code analysis */
+
+/* Properties of a code (weight, distance, minimum distance, linear [n,k]
+ * codes; :123 orthogonality), computed on the GPU:
+ *   weight_hist[w]   number of words of weight w
+ *   gf2_rank         dimension of the span; is_linear = (M == 2^gf2_rank) (distinct words)
+ *   min_distance     GC_ANALYZE_PAIRWISE: min over all pairs of popcount(u ^ v) (M(M-1)/2
+ *                    XOR+POPC checks, the screen's kernel shape); otherwise, for a linear
+ *                    code, the minimum nonzero weight; 0 if undetermined or M < 2
+ *   self_orthogonal  1 every pair (and word) has even AND-parity, 0 not, 2 undetermined
+ *                    (nonlinear code without GC_ANALYZE_PAIRWISE | GC_ANALYZE_ORTHOGONALITY) */
+typedef struct gc_analysis {
+    uint32_t struct_size;
+    uint32_t min_distance;
+    uint64_t M;
+    uint64_t weight_hist[33];
+    uint32_t gf2_rank;
+    uint32_t is_linear;
+    uint32_t self_orthogonal;
+    uint32_t reserved;
+    uint64_t pairs_checked;
+} gc_analysis;
+#define GC_ANALYZE_PAIRWISE      0x1u
+#define GC_ANALYZE_ORTHOGONALITY 0x2u   /* with PAIRWISE: AND-parity of every pair too */
+
+/* d_words: DEVICE array of M 32-bit words; synchronises `stream`.  GC_EINVAL for NULL
+ * pointers (d_words may be NULL iff M == 0) or unknown flags. */
+int gc_analyze_device(const uint32_t *d_words, uint64_t M, uint32_t flags, void *stream, gc_analysis *out);
+/* words: HOST array of M words < 2^32 (copied to the device). */
+int gc_analyze(const uint64_t *words, uint64_t M, uint32_t flags, gc_analysis *out);
+
 /* Upper bound on M: the sphere-packing (Hamming) bound for (n, d); for even d the
  * bound of (n-1, d-1) (a code of even distance d and length n punctures to one of
  * length n-1 and distance d-1).  Clamped to 2^n.  Returns 0 if the arguments are invalid.

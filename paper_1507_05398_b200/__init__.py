@@ -29,6 +29,8 @@ from ._binding import (  # noqa: F401
     exported_symbols,
     gc_abi_version,
     GcComm,
+    gc_analyze,
+    gc_analyze_device,
     gc_capacity_bound,
     gc_comm_create,
     gc_comm_destroy,

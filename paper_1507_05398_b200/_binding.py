@@ -60,6 +60,22 @@ class gc_stats(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_ if name != "struct_size"}
 
 
+class gc_analysis(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("min_distance", ctypes.c_uint32), ("M", ctypes.c_uint64),
+                ("weight_hist", ctypes.c_uint64 * 33), ("gf2_rank", ctypes.c_uint32),
+                ("is_linear", ctypes.c_uint32), ("self_orthogonal", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32), ("pairs_checked", ctypes.c_uint64)]
+
+    def to_dict(self) -> dict:
+        return {"M": self.M, "min_distance": self.min_distance, "gf2_rank": self.gf2_rank,
+                "is_linear": bool(self.is_linear), "self_orthogonal": {0: False, 1: True}.get(self.self_orthogonal),
+                "weights": {w: int(self.weight_hist[w]) for w in range(33) if self.weight_hist[w]},
+                "pairs_checked": self.pairs_checked}
+
+
+GC_ANALYZE_PAIRWISE = 0x1
+GC_ANALYZE_ORTHOGONALITY = 0x2
+
 _u64p = ctypes.POINTER(ctypes.c_uint64)
 _u32p = ctypes.POINTER(ctypes.c_uint32)
 _u8p = ctypes.POINTER(ctypes.c_uint8)
@@ -99,6 +115,9 @@ _sig("gc_generate_rank", ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, ctypes
                                         ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.POINTER(gc_stats)])
 _sig("gc_tile_partition", ctypes.c_int, [ctypes.c_uint32, ctypes.c_int, ctypes.c_int, _u32p, _u32p, _u32p])
+_sig("gc_analyze", ctypes.c_int, [_u64p, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(gc_analysis)])
+_sig("gc_analyze_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p,
+                                         ctypes.POINTER(gc_analysis)])
 _sig("gc_strerror", ctypes.c_char_p, [ctypes.c_int])
 _sig("gc_last_error", ctypes.c_char_p, [])
 _sig("gc_abi_version", ctypes.c_int, [])
@@ -250,6 +269,30 @@ def gc_construct_device(n: int, d: int, codebook, count, ordering="lex", basis=N
                                     _stream_ptr(stream), _ref(st)), "gc_construct_device")
     del keep
     return st.to_dict() if st is not None else None
+
+
+def gc_analyze(words, pairwise: bool = False, orthogonality: bool = False) -> dict:
+    """Code analysis on the GPU (gc_analyze): weight distribution, GF(2) rank, linearity,
+    minimum distance (pairwise or, for linear codes, min nonzero weight), self-orthogonality."""
+    w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64))
+    a = gc_analysis()
+    a.struct_size = ctypes.sizeof(gc_analysis)
+    flags = (GC_ANALYZE_PAIRWISE if pairwise else 0) | (GC_ANALYZE_ORTHOGONALITY if orthogonality else 0)
+    _check(_lib.gc_analyze(w.ctypes.data_as(_u64p) if len(w) else None, len(w), flags, ctypes.byref(a)),
+           "gc_analyze")
+    return a.to_dict()
+
+
+def gc_analyze_device(words, M: int | None = None, pairwise: bool = False, orthogonality: bool = False,
+                      stream=None) -> dict:
+    """As gc_analyze for a CUDA tensor of 32-bit words."""
+    a = gc_analysis()
+    a.struct_size = ctypes.sizeof(gc_analysis)
+    M = words.numel() * words.element_size() // 4 if M is None else M
+    flags = (GC_ANALYZE_PAIRWISE if pairwise else 0) | (GC_ANALYZE_ORTHOGONALITY if orthogonality else 0)
+    _check(_lib.gc_analyze_device(words.data_ptr() if M else None, M, flags, _stream_ptr(stream), ctypes.byref(a)),
+           "gc_analyze_device")
+    return a.to_dict()
 
 
 def gc_rank_to_vector(ordering, n: int, rank: int) -> int:

@@ -63,6 +63,8 @@ struct RunArgs {
 };
 int engine_run(const RunArgs &a);
 int gc_problem_to_args(const gc_problem *p, RunArgs *a);   // gc_abi.cpp (validation, no CUDA)
+int analyze_device(const uint32_t *d_words, uint64_t M, int pairwise, int orth, void *stream,
+                   gc_analysis *out);                        // gc_analysis.cu
 bool persistent_supported(const RunArgs &a);   // gc_persistent.cu
 int persistent_run(const RunArgs &a);
 int engine_ranks_to_vectors_device(int ordering, uint32_t n, uint64_t first, uint64_t count,
