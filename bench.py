@@ -39,8 +39,41 @@ CHECK_PEAK_PER_CLK_SM = {"popc": 15.49, 2: 23.62, 3: 19.18, 4: 16.66}
 
 
 def parse_workload(s: str):
-    n, d, o = s.split(",")
-    return int(n), int(d), o
+    """n,d,ordering[,so][,cw=W][,basis=gray|std|seed:S] -> (n, d, ordering, extras)."""
+    parts = s.split(",")
+    n, d, o = int(parts[0]), int(parts[1]), parts[2]
+    ex = {}
+    for p in parts[3:]:
+        if p == "so":
+            ex["self_orthogonal"] = True
+        elif p.startswith("cw="):
+            ex["constant_weight"] = int(p[3:])
+        elif p.startswith("basis="):
+            kind = p[6:]
+            if kind == "gray":
+                ex["basis"] = [1] + [3 << (j - 1) for j in range(1, n)]
+            elif kind == "std":
+                ex["basis"] = [1 << j for j in range(n)]
+            elif kind.startswith("seed:"):
+                import random
+                rng = random.Random(int(kind[5:]))
+                while True:   # random invertible basis (seeded)
+                    b = [rng.randrange(1, 1 << n) for _ in range(n)]
+                    red = {}
+                    for x in b:
+                        while x:
+                            h = x.bit_length() - 1
+                            if h in red:
+                                x ^= red[h]
+                            else:
+                                red[h] = x
+                                break
+                    if len(red) == n:
+                        ex["basis"] = b
+                        break
+        else:
+            raise ValueError(f"unknown workload option {p}")
+    return n, d, o, ex
 
 
 def measured_peaks():
@@ -154,9 +187,12 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    n, d, o = parse_workload(args.workload)
+    n, d, o, ex = parse_workload(args.workload)
     import numpy as np
     import oracle as O
+    if ex:
+        print(json.dumps({"impl": "reference", "unavailable": "the reference arm times the base greedy only"}))
+        return 0
     k = min(args.ref_log2, n)
     nranks = 1 << k
     table = O.order_table(o, k) if o in ("lex", "gray") else O.order_table(o, n)[:nranks].copy()
@@ -221,6 +257,9 @@ def run_b200(args):
     opts = {"flags": gc.GC_FLAG_KERNEL_TIMING}
 
     def construct():
+        if ex:
+            return gc.gc_construct_device(n, d, codebook, count, ordering=o, stream=stream, options=opts,
+                                          stats=True, **ex)
         return gc.gc_generate_rank(n, d, o, comm, codebook, count, stream=stream, options=opts)
 
     def barrier():
@@ -251,10 +290,32 @@ def run_b200(args):
     M = int(count.item())
     w_def = stats[-1]["w_def"]
     value = w_def / (ms_per_step * 1e-3)
+    if ex:
+        # filtered problems have no definitional count over all ranks: report executed checks/s
+        value = stats[-1]["checks_exec"] / (ms_per_step * 1e-3)
+        if e2e_val is not None:
+            e2e_val = stats[-1]["checks_exec"] / (e2e_val * 1e-3)
 
     # e2e through the public API: host buffers, device->host copy of the code inside the region
     e2e_val, d2h = None, 0
-    if world == 1:
+    if world == 1 and ex:
+        e2e_val = None            # the host-buffer entry for extended problems is gc_construct
+        gc.gc_construct(n, d, ordering=o, **ex)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ds = torch.cuda.default_stream(dev)
+        tot = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            e0.record(ds)
+            w, _ = gc.gc_construct(n, d, ordering=o, **ex)
+            e1.record(ds)
+            torch.cuda.synchronize(dev)
+            tot += e0.elapsed_time(e1)
+            d2h = w.nbytes
+        e2e_val = (tot / args.steps)
+    elif world == 1:
         gc.gc_generate(n, d, o)       # warm (allocations)
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -306,7 +367,7 @@ def run_b200(args):
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (the whole space F_2^n in the chosen ordering; no dataset)",
-            "config": {"workload": f"n={n},d={d},{o}", "M": M, "w_def": w_def,
+            "config": {"workload": args.workload, "M": M, "w_def": w_def,
                        "parallelism": f"candidate-partitioned x{world}, replicated codebook",
                        "l2": "flushed between timed steps (512 MiB write)"},
             "w_exec": checks / args.steps,
@@ -323,7 +384,9 @@ def run_b200(args):
             "gpu_launches": int(sum(s["launches"] for s in stats)),
             "clocks": clocks,
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if ex:
+            line["metric"] = "executed candidate-codeword checks/sec (W_exec; constrained problem)"
+        if world == 1 and not args.no_cpu_baseline and not ex:
             v, desc = oracle_sample(n, d, o, budget_s=args.cpu_budget)
             line["cpu_baseline"] = {"value": v, "unit": "checks/s", "cores": 1, "kind": "oracle", "sample": desc}
         print(json.dumps(line), flush=True)
