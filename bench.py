@@ -243,7 +243,7 @@ def run_b200(args):
         return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    n, d, o = parse_workload(args.workload)
+    n, d, o, ex = parse_workload(args.workload)
     from paper_1507_05398_b200 import dist as gdist
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
