@@ -43,6 +43,7 @@ constexpr uint32_t kPMaxTile = 1u << 16;    // largest tile (tile indices fit in
 // survivors resolved per chunk (shared memory): 4096 with one CTA per SM, 2048 with two
 constexpr uint32_t kPMaxBatches = kPMaxTile / 32;
 constexpr uint32_t kPTargetAccepted = 128;  // adaptive tiles grow up to ~2x this many accepted words
+constexpr uint32_t kPMaxPredictedSurvivors = 1024;
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + s_adjn (1 B) + s_adj (2 B x kPAdj)
 __host__ __device__ constexpr size_t p_resolve_smem(uint32_t chunk) { return (size_t)chunk * (8 + 2 * kPAdj); }
@@ -66,6 +67,7 @@ struct PState {
     unsigned long long n_overflow, n_seq, n_rounds;
     unsigned int error;
     unsigned int K_next;                       // size of the next tile (set by CTA 0)
+    unsigned int S_last, K_last;               // last tile with survivors: its S and K
     unsigned int wfirst[33];                   // graded orders: 1 + index of the first codeword of weight w
 };
 
@@ -107,10 +109,15 @@ struct PArgs {
 //   and grows back toward cap while S <= 9/8 A.
 // Deterministic: a function of (K, S, A, t1, M1) only, never of timing.
 __device__ __forceinline__ uint32_t p_next_tile(const PArgs &a, uint32_t K, uint32_t S, uint32_t A,
-                                                unsigned long long t1, unsigned long long M1) {
+                                                unsigned long long t1, unsigned long long M1,
+                                                uint32_t S_last, uint32_t K_last) {
     const unsigned long long want = M1 ? (unsigned long long)kPTargetAccepted * t1 / M1 : ~0ull;
     uint32_t cap = a.tile_min;
-    while (cap < a.tile_max && (unsigned long long)cap * 2 <= want && (unsigned long long)cap * 16 <= t1) cap <<= 1;
+    // survivors predicted from the last tile that had any (bursty orders, e.g. graded ones at
+    // large d, have long empty stretches): keep them <= kPMaxPredictedSurvivors
+    while (cap < a.tile_max && (unsigned long long)cap * 2 <= want && (unsigned long long)cap * 16 <= t1 &&
+           (unsigned long long)S_last * cap * 2 <= (unsigned long long)kPMaxPredictedSurvivors * K_last)
+        cap <<= 1;
     uint32_t Kn = K;
     if (A > 0 && (unsigned long long)S * 4 > (unsigned long long)A * 5) Kn = K > a.tile_min ? K / 2 : K;
     else if (A == 0 || (unsigned long long)S * 8 <= (unsigned long long)A * 9) Kn = K * 2;
@@ -669,7 +676,8 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                             if (!st->wfirst[w]) st->wfirst[w] = (unsigned int)(p + 1);
                     }
                 }
-                st->K_next = p_next_tile(a, K, S, A, t0 + K, M1);
+                if (S) { st->S_last = S; st->K_last = K; }
+                st->K_next = p_next_tile(a, K, S, A, t0 + K, M1, st->S_last, st->K_last ? st->K_last : 1u);
                 st->survivors += S;
                 st->tiles += 1;
                 st->levels += L;
