@@ -62,6 +62,7 @@ struct PState {
     unsigned long long tiles;
     unsigned long long levels;
     unsigned long long t_level[kPMaxLevels];   // diagnostics: CTA 0's view, ns (%globaltimer)
+    unsigned long long c_level[kPMaxLevels];   // diagnostics: lane-checks per level
     unsigned long long t_resolve, t_sync, t_tile;
     unsigned long long t_r[6];                 // resolve sub-steps
     unsigned long long n_overflow, n_seq, n_rounds;
@@ -80,6 +81,7 @@ struct PArgs {
     int mix;                        // 2..4: half the checks via p_clear_low<d> (d <= 4), 0: POPC only
     uint32_t chunk;                 // survivors per resolve chunk
     int weight_bound;               // graded orders: stop the screen at the weight bound
+    int items_per_warp;             // target work items per warp and level
     // SURVEY 8(f) extensions
     int use_basis;                  // B-ordering: rank -> XOR of basis[j] over set bits j
     uint32_t basis[32];
@@ -451,13 +453,14 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             long long sub = 0;
             uint32_t nsub = 0;
             if (wlen > 0 && B > 0) {
-                const long long want = ((long long)nwarps * 4 + B - 1) / B;     // sub-ranges wanted
+                const long long want = ((long long)nwarps * a.items_per_warp + B - 1) / B;   // sub-ranges wanted
                 sub = (wlen + want - 1) / want;
                 sub = (sub + 31) & ~31ll;
                 sub = max(sub, (long long)kPSubMin);
                 sub = min(sub, (long long)kPSubMax);
                 nsub = (uint32_t)((wlen + sub - 1) / sub);
             }
+            const unsigned long long checks_before = my_checks;
             PLevel lv;
             lv.l = l; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
             lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0;
@@ -477,6 +480,11 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                 } else {
                     p_item<1, 0>(a, lv, it, C, off, my_checks);
                 }
+            }
+            if (a.timing) {
+                unsigned long long dc = my_checks - checks_before;
+                for (int o = 16; o > 0; o >>= 1) dc += __shfl_down_sync(0xffffffffu, dc, o);
+                if ((threadIdx.x & 31) == 0 && dc) atomicAdd(&st->c_level[l], dc);
             }
             grid.sync();
             if (timer) { const unsigned long long t = p_now(); st->t_level[l] += t - tm; tm = t; }
@@ -786,6 +794,7 @@ int persistent_run(const RunArgs &r) {
     a.q0 = cx->q0; a.q1 = cx->q1; a.surv = cx->surv; a.status = cx->status;
     a.st = cx->st; a.d_count = (unsigned long long *)r.d_count;
     a.timing = getenv("GC_DEBUG_PHASES") != nullptr;
+    a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP"))) : 2;
     a.use_basis = r.use_basis;
     for (int i = 0; i < 32; ++i) a.basis[i] = r.basis[i];
     a.so = r.self_orthogonal;
@@ -851,8 +860,10 @@ int persistent_run(const RunArgs &r) {
                     full.n_overflow / T, full.n_rounds / T, full.n_seq / T);
             for (int l = 0; l < kPMaxLevels; ++l)
                 if (full.t_level[l])
-                    fprintf(stderr, "[gc]   level %2d: %.3f s total (%.2f us per tile)\n", l, full.t_level[l] / 1e9,
-                            full.t_level[l] / T / 1e3);
+                    fprintf(stderr, "[gc]   level %2d: %.3f s total (%.2f us per tile), %.3g checks, %.1f%% of the "
+                            "mixed/POPC peak (148 SM x 19.18/clk x 1965 MHz)\n", l, full.t_level[l] / 1e9,
+                            full.t_level[l] / T / 1e3, (double)full.c_level[l],
+                            100.0 * (double)full.c_level[l] / (full.t_level[l] * 1e-9) / (148.0 * 19.18 * 1.965e9));
         }
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }
