@@ -522,6 +522,12 @@ static int phases_for(unsigned long long M_ub, uint32_t W0, uint32_t growth) {
 
 int engine_run(const RunArgs &a) {
     auto wall0 = std::chrono::steady_clock::now();
+    if (persistent_partitioned_supported(a)) {
+        int rc = persistent_run_partitioned(a);
+        if (a.stats) a.stats->wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+        return rc;
+    }
     if (a.extended() && !persistent_supported(a)) {
         set_error("B-ordering / self-orthogonal / constant-weight problems run on the single-GPU persistent "
                   "engine only (no emulate_ranks, launched tiles, no-early-exit or sequential-resolve flags)");

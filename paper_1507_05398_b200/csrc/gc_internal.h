@@ -67,6 +67,8 @@ int analyze_device(const uint32_t *d_words, uint64_t M, int pairwise, int orth, 
                    gc_analysis *out);                        // gc_analysis.cu
 bool persistent_supported(const RunArgs &a);   // gc_persistent.cu
 int persistent_run(const RunArgs &a);
+bool persistent_partitioned_supported(const RunArgs &a);
+int persistent_run_partitioned(const RunArgs &a);
 int engine_ranks_to_vectors_device(int ordering, uint32_t n, uint64_t first, uint64_t count,
                                    uint32_t *d_out, void *stream);
 

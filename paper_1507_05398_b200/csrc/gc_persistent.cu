@@ -82,6 +82,11 @@ struct PArgs {
     uint32_t chunk;                 // survivors per resolve chunk
     int weight_bound;               // graded orders: stop the screen at the weight bound
     int items_per_warp;             // target work items per warp and level
+    // partition mode (multi-GPU / emulated ranks): one tile's screen over one candidate range
+    int part_mode;
+    unsigned long long t_single;
+    uint32_t K_single, part_lo, part_len;
+    int vals_valid;                 // a.vals holds every candidate of the tile (else regenerate)
     // SURVEY 8(f) extensions
     int use_basis;                  // B-ordering: rank -> XOR of basis[j] over set bits j
     uint32_t basis[32];
@@ -274,6 +279,8 @@ struct PLevel {
     const uint32_t *s_live;  // level >= 1: live bits per mask word (smem)
     uint32_t words;
     const uint32_t *basis;   // B-ordering basis (smem)
+    uint32_t c_lo;           // first tile index of the screened range
+    uint32_t w_base;         // 32 * (first mask word of the range)
 };
 
 // tile index of the q-th live candidate of level >= 1 (q < n_l): the mask word w with
@@ -286,7 +293,7 @@ __device__ __forceinline__ uint32_t p_locate(const PLevel &lv, uint32_t q) {
     }
     uint32_t bits = lv.s_live[lo];
     for (uint32_t k = q - lv.s_pre[lo]; k > 0; --k) bits &= bits - 1;
-    return lo * 32 + (__ffs(bits) - 1);
+    return lv.w_base + lo * 32 + (__ffs(bits) - 1);
 }
 
 // One warp item: batch b (32 R candidates) of the level's live candidates against sub-range
@@ -312,9 +319,9 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
         idx[r] = 0; v[r] = 0;
         if (live[r]) {
             if (lv.l == 0) {
-                idx[r] = q;
-                v[r] = p_gen(a, C, off, lv.basis, lv.t0 + q);
-                if (j == 0) a.vals[q] = v[r];
+                idx[r] = lv.c_lo + q;
+                v[r] = p_gen(a, C, off, lv.basis, lv.t0 + idx[r]);
+                if (j == 0) a.vals[idx[r]] = v[r];
                 if (!p_allowed(a, v[r])) { filtered[r] = true; live[r] = false; }
             } else {
                 idx[r] = p_locate(lv, q);
@@ -361,6 +368,246 @@ __device__ __forceinline__ unsigned long long p_now() {
     return t;
 }
 
+// a3 + a4 for one tile, by ONE CTA: survivors in rank order (from the dead mask), in-tile
+// ordered resolve, ordered append, M += A, next tile size, per-tile state cleared.
+// first codeword the tile must be screened against (weight bound, graded orders), else 0
+__device__ __forceinline__ unsigned long long p_base(const PArgs &a, unsigned long long t0, unsigned long long M) {
+    if (!a.weight_bound) return 0;
+    int w_lo = 0;
+    while (t0 >= a.tabs->off[w_lo + 1]) ++w_lo;
+    for (int w = max(0, w_lo - (int)a.d + 1); w <= a.n; ++w) {
+        const unsigned int f = __ldcg(&a.st->wfirst[w]);
+        if (f) return f - 1;
+    }
+    return M;
+}
+
+struct PSmem {
+    const uint32_t (*C)[33];
+    const uint64_t *off;
+    const uint32_t *s_basis;
+    uint32_t *s_ws, *s_val;
+    uint16_t *s_idx;
+    uint8_t *s_status, *s_adjn;
+    uint16_t *s_adj;
+    uint32_t chunk;
+};
+
+__device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsigned long long t0, uint32_t K, int L,
+                                       bool timer, unsigned long long tm) {
+    const uint32_t kPChunk = sm.chunk;
+    const uint32_t (*C)[33] = sm.C;
+    const uint64_t *off = sm.off;
+    const uint32_t *s_basis = sm.s_basis;
+    uint32_t *s_ws = sm.s_ws, *s_val = sm.s_val;
+    uint16_t *s_idx = sm.s_idx;
+    uint8_t *s_status = sm.s_status, *s_adjn = sm.s_adjn;
+    uint16_t *s_adj = sm.s_adj;
+    PState *st = a.st;
+    const int lane = threadIdx.x & 31;
+    const uint32_t words = (K + 31) / 32;
+        const uint32_t tid = threadIdx.x;
+        if (L == 0) {      // empty codebook: no level generated the candidates
+            for (uint32_t i = tid; i < K; i += blockDim.x) {
+                const uint32_t v = p_gen(a, C, off, s_basis, t0 + i);
+                a.vals[i] = v;
+                if (!p_allowed(a, v)) atomicOr(&a.dead[i >> 5], 1u << (i & 31));
+            }
+            __syncthreads();
+        }
+        // survivors in rank order -> a.surv (global; S <= K)
+        uint32_t S = 0;
+        for (uint32_t w0 = 0; w0 < words; w0 += blockDim.x) {
+            const uint32_t w = w0 + tid;
+            uint32_t alive = 0;
+            if (w < words) {
+                alive = ~__ldcg(a.dead + w);
+                if (w * 32 + 32 > K) alive &= (1u << (K - w * 32)) - 1u;
+            }
+            uint32_t tot;
+            uint32_t pos = S + p_block_scan(__popc(alive), &tot, s_ws);
+            while (alive) {
+                const int bit = __ffs(alive) - 1;
+                alive &= alive - 1;
+                const uint32_t i = w * 32 + bit;
+                a.surv[pos++] = make_uint2(i, a.vals_valid ? __ldcg(a.vals + i) : p_gen(a, C, off, s_basis, t0 + i));
+            }
+            S += tot;
+        }
+        __syncthreads();
+        unsigned long long tr = timer ? p_now() : 0;
+#define P_TR(i) if (timer) { const unsigned long long t_ = p_now(); st->t_r[i] += t_ - tr; tr = t_; }
+        if (timer) st->t_r[0] += tr - tm;
+        __shared__ unsigned long long s_stat[3];
+        if (tid < 3) s_stat[tid] = 0;
+        __syncthreads();
+        unsigned long long rchk = 0, confl = 0, wdef = 0;
+        const unsigned long long M0 = __ldcg(&st->M);
+        uint32_t A = 0;                   // accepted so far in this tile (codebook[M0, M0+A))
+        for (uint32_t c0 = 0; c0 < S; c0 += kPChunk) {
+            const uint32_t Sc = min(kPChunk, S - c0);
+            for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                const uint2 e = __ldcg(a.surv + c0 + j);
+                s_idx[j] = (uint16_t)e.x;
+                s_val[j] = e.y;
+            }
+            __syncthreads();
+            // in-chunk conflicts: s_adj[j] lists (up to kPAdj) earlier survivors of the chunk
+            // within distance < d (s_adjn = 255: more); survivors conflicting with a word
+            // accepted in an earlier chunk of this tile are rejected outright.
+            // status 1 = accepted, 0 = rejected, 2 = undecided.
+            for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                const uint32_t vj = s_val[j];
+                bool prev = false;
+                for (uint32_t t = 0; t < A && !prev; ++t)
+                    prev = p_conflict(a, vj, __ldcg(a.codebook + M0 + t));
+                uint32_t cnt = 0;
+                // 32 earlier survivors at a time: independent loads/checks into a bit mask,
+                // then record the (rare) conflicts
+                for (uint32_t k0 = 0; k0 < j; k0 += 32) {
+                    const uint32_t kn = min(32u, j - k0);
+                    uint32_t mask = 0;
+                    if (kn == 32) {
+#pragma unroll
+                        for (int t = 0; t < 32; ++t)
+                            mask |= (uint32_t)p_conflict(a, vj, s_val[k0 + t]) << t;
+                    } else {
+                        for (uint32_t t = 0; t < kn; ++t)
+                            mask |= (uint32_t)p_conflict(a, vj, s_val[k0 + t]) << t;
+                    }
+                    while (mask) {
+                        const uint32_t t = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        if (cnt < kPAdj) s_adj[j * kPAdj + cnt] = (uint16_t)(k0 + t);
+                        ++cnt;
+                    }
+                }
+                rchk += j + A;
+                s_adjn[j] = cnt > kPAdj ? 255 : (uint8_t)cnt;
+                if (a.timing && cnt > kPAdj) atomicAdd(&st->n_overflow, 1ull);
+                s_status[j] = prev ? 0 : (cnt ? 2 : 1);
+                confl += cnt;
+            }
+            __syncthreads();
+            P_TR(1)
+            // Parallel rounds: an undecided survivor is rejected as soon as one earlier
+            // conflicting survivor is accepted, accepted once all of them are rejected.  Long
+            // dependency chains are finished by warp 0 walking the undecided ones in rank
+            // order.  A survivor is accepted iff no earlier ACCEPTED survivor conflicts.
+            int left = 0;
+            for (int round = 0; round < 8; ++round) {
+                int undecided = 0;
+                for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                    if (s_status[j] != 2) continue;
+                    const uint32_t na = s_adjn[j];
+                    bool acc_nb = false, und_nb = false;
+                    if (na != 255) {
+                        for (uint32_t t = 0; t < na; ++t) {
+                            const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
+                            acc_nb |= sk == 1;
+                            und_nb |= sk == 2;
+                        }
+                    } else {
+                        const uint32_t vj = s_val[j];
+                        for (uint32_t k = 0; k < j; ++k) {
+                            if (p_conflict(a, vj, s_val[k])) {
+                                const uint8_t sk = s_status[k];
+                                acc_nb |= sk == 1;
+                                und_nb |= sk == 2;
+                            }
+                        }
+                    }
+                    // a status read in the same round may be stale (2): that only delays
+                    if (acc_nb) s_status[j] = 0;
+                    else if (!und_nb) s_status[j] = 1;
+                    else undecided = 1;
+                }
+                if (a.timing && tid == 0) atomicAdd(&st->n_rounds, 1ull);
+                left = __syncthreads_or(undecided);
+                if (!left) break;
+            }
+            if (left && tid < 32) {
+                for (uint32_t j = 0; j < Sc; ++j) {
+                    if (s_status[j] != 2) continue;                 // warp-uniform
+                    if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
+                    const uint32_t na = s_adjn[j];
+                    bool acc_nb = false;
+                    if (na != 255) {
+                        if (lane < na) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
+                    } else {
+                        const uint32_t vj = s_val[j];
+                        for (uint32_t k = lane; k < j; k += 32)
+                            acc_nb |= (s_status[k] == 1) && p_conflict(a, vj, s_val[k]);
+                    }
+                    acc_nb = __any_sync(0xffffffffu, acc_nb);
+                    if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+            P_TR(2)
+            // ordered append of the chunk's accepted survivors
+            for (uint32_t j0 = 0; j0 < Sc; j0 += blockDim.x) {
+                const uint32_t j = j0 + tid;
+                const uint32_t acc = (j < Sc && s_status[j] == 1) ? 1u : 0u;
+                uint32_t tot;
+                const uint32_t pos = A + p_block_scan(acc, &tot, s_ws);
+                if (acc) {
+                    if (M0 + pos < a.capacity) a.codebook[M0 + pos] = s_val[j];
+                    else st->error = 1;
+                    if (a.wdef_valid) wdef += a.N - 1 - (t0 + s_idx[j]);
+                }
+                A += tot;
+            }
+            if (A > a.capacity - M0) A = (uint32_t)(a.capacity - M0);
+            __threadfence_block();
+            __syncthreads();
+            P_TR(3)
+        }
+        // clear per-tile state for the next tile
+        for (uint32_t w = tid; w < words; w += blockDim.x) a.dead[w] = 0;
+        // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            rchk += __shfl_down_sync(0xffffffffu, rchk, o);
+            confl += __shfl_down_sync(0xffffffffu, confl, o);
+            wdef += __shfl_down_sync(0xffffffffu, wdef, o);
+        }
+        if (lane == 0) {
+            if (rchk) atomicAdd(&s_stat[0], rchk);
+            if (confl) atomicAdd(&s_stat[1], confl);
+            if (wdef) atomicAdd(&s_stat[2], wdef);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            st->resolve_checks += s_stat[0];
+            st->conflicts += s_stat[1];
+            st->w_def += s_stat[2];
+        }
+        P_TR(4)
+        if (tid == 0) {
+            unsigned long long M1 = M0 + A;
+            if (M1 > a.capacity) M1 = a.capacity;
+            st->M = M1;
+            if (a.weight_bound) {
+                // first index of each weight among the words just appended (acceptance
+                // order is weight-sorted for graded orders); stored +1, 0 = none yet
+                for (unsigned long long p = M0; p < M1; ++p) {
+                    const uint32_t w = __popc(a.codebook[p]);
+                    if (p == 0 || __popc(a.codebook[p - 1]) != w)
+                        if (!st->wfirst[w]) st->wfirst[w] = (unsigned int)(p + 1);
+                }
+            }
+            if (S) { st->S_last = S; st->K_last = K; }
+            st->K_next = p_next_tile(a, K, S, A, t0 + K, M1, st->S_last, st->K_last ? st->K_last : 1u);
+            st->survivors += S;
+            st->tiles += 1;
+            st->levels += L;
+        }
+        __threadfence();
+    
+}
+
 template <int kMinBlocks>
 __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     const uint32_t kPChunk = a.chunk;
@@ -389,27 +636,25 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     const uint32_t gwarp = blockIdx.x * kPWarps + (threadIdx.x >> 5);
     const uint32_t nwarps = gridDim.x * kPWarps;
     unsigned long long my_checks = 0;
+    PSmem sm;
+    sm.C = C; sm.off = off; sm.s_basis = s_basis; sm.s_ws = s_ws; sm.s_val = s_val; sm.s_idx = s_idx;
+    sm.s_status = s_status; sm.s_adjn = s_adjn; sm.s_adj = s_adj; sm.chunk = kPChunk;
 
-    unsigned long long t0 = a.t_begin;
+    unsigned long long t0 = a.part_mode ? a.t_single : a.t_begin;
     while (t0 < a.t_end) {
         const unsigned long long M = __ldcg(&st->M);
-        uint32_t K = __ldcg(&st->K_next);
+        uint32_t K = a.part_mode ? a.K_single : __ldcg(&st->K_next);
         if ((unsigned long long)K > a.t_end - t0) K = (uint32_t)(a.t_end - t0);
+        // candidate range screened by this launch: the tile, or one rank's partition of it
+        const uint32_t c_lo = a.part_mode ? min(a.part_lo, K) : 0u;
+        const uint32_t c_hi = a.part_mode ? min(a.part_lo + a.part_len, K) : K;
+        const uint32_t w_lo = c_lo / 32;
         // Weight bound (graded orders, GC_FLAG_NO_WEIGHT_BOUND unset): the codebook is sorted
         // by weight and |wt(v) - wt(c)| <= dist(v, c), so codewords of weight < w_lo - (d-1)
         // (w_lo = weight of the tile's first candidate) are at distance >= d from every
         // candidate of the tile: the screen stops at the first codeword of weight
         // >= w_lo - d + 1.  Exact -- only checks whose outcome is known are skipped.
-        unsigned long long base = 0;
-        if (a.weight_bound) {
-            int w_lo = 0;
-            while (t0 >= a.tabs->off[w_lo + 1]) ++w_lo;
-            base = M;
-            for (int w = max(0, w_lo - (int)a.d + 1); w <= a.n; ++w) {
-                const unsigned int f = __ldcg(&st->wfirst[w]);
-                if (f) { base = f - 1; break; }
-            }
-        }
+        const unsigned long long base = p_base(a, t0, M);
         const int L = p_levels(M - base, a.W0, a.growth);
         const uint32_t W0 = a.W0;
         const bool timer = a.timing && blockIdx.x == 0 && threadIdx.x == 0;
@@ -424,23 +669,26 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             if (lo < (long long)base) lo = (long long)base;
             // live candidates of this level: level 0 all K; deeper levels from the dead mask,
             // compacted through a per-CTA prefix over the mask words (every CTA builds it)
-            uint32_t n_l = K;
+            uint32_t n_l = c_hi - c_lo;
+            const uint32_t pwords = (c_hi + 31) / 32 - w_lo;      // mask words of the range
             if (l > 0) {
                 uint32_t tot_all = 0;
-                for (uint32_t w0 = 0; w0 < words; w0 += blockDim.x) {
-                    const uint32_t w = w0 + threadIdx.x;
+                for (uint32_t w0 = 0; w0 < pwords; w0 += blockDim.x) {
+                    const uint32_t wr = w0 + threadIdx.x;          // relative word
                     uint32_t live = 0;
-                    if (w < words) {
+                    if (wr < pwords) {
+                        const uint32_t w = w_lo + wr;
                         live = ~__ldcg(a.dead + w);
-                        if (w * 32 + 32 > K) live &= (1u << (K - w * 32)) - 1u;
-                        s_live[w] = live;
+                        if (w * 32 + 32 > c_hi) live &= (1u << (c_hi - w * 32)) - 1u;
+                        if (w * 32 < c_lo) live &= ~((1u << (c_lo - w * 32)) - 1u);
+                        s_live[wr] = live;
                     }
                     uint32_t tot;
                     const uint32_t pre = tot_all + p_block_scan(__popc(live), &tot, s_ws);
-                    if (w < words) s_pre[w] = pre;
+                    if (wr < pwords) s_pre[wr] = pre;
                     tot_all += tot;
                 }
-                if (threadIdx.x == 0) s_pre[words] = tot_all;
+                if (threadIdx.x == 0) s_pre[pwords] = tot_all;
                 __syncthreads();
                 n_l = tot_all;
             }
@@ -464,7 +712,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             PLevel lv;
             lv.l = l; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
             lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0;
-            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = words; lv.basis = s_basis;
+            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = pwords; lv.basis = s_basis; lv.c_lo = c_lo; lv.w_base = w_lo * 32;
             const unsigned long long items = (unsigned long long)B * nsub;
             for (unsigned long long it = gwarp; it < items; it += nwarps) {
                 if (a.so) {
@@ -490,208 +738,9 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             if (timer) { const unsigned long long t = p_now(); st->t_level[l] += t - tm; tm = t; }
         }
 
+        if (a.part_mode) break;       // the host runs the exchange and k_resolve_tile
         // ------------------------------------------------ resolve + commit (CTA 0)
-        if (blockIdx.x == 0) {
-            const uint32_t tid = threadIdx.x;
-            if (L == 0) {      // empty codebook: no level generated the candidates
-                for (uint32_t i = tid; i < K; i += blockDim.x) {
-                    const uint32_t v = p_gen(a, C, off, s_basis, t0 + i);
-                    a.vals[i] = v;
-                    if (!p_allowed(a, v)) atomicOr(&a.dead[i >> 5], 1u << (i & 31));
-                }
-                __syncthreads();
-            }
-            // survivors in rank order -> a.surv (global; S <= K)
-            uint32_t S = 0;
-            for (uint32_t w0 = 0; w0 < words; w0 += blockDim.x) {
-                const uint32_t w = w0 + tid;
-                uint32_t alive = 0;
-                if (w < words) {
-                    alive = ~__ldcg(a.dead + w);
-                    if (w * 32 + 32 > K) alive &= (1u << (K - w * 32)) - 1u;
-                }
-                uint32_t tot;
-                uint32_t pos = S + p_block_scan(__popc(alive), &tot, s_ws);
-                while (alive) {
-                    const int bit = __ffs(alive) - 1;
-                    alive &= alive - 1;
-                    const uint32_t i = w * 32 + bit;
-                    a.surv[pos++] = make_uint2(i, __ldcg(a.vals + i));
-                }
-                S += tot;
-            }
-            __syncthreads();
-            unsigned long long tr = timer ? p_now() : 0;
-#define P_TR(i) if (timer) { const unsigned long long t_ = p_now(); st->t_r[i] += t_ - tr; tr = t_; }
-            if (timer) st->t_r[0] += tr - tm;
-            __shared__ unsigned long long s_stat[3];
-            if (tid < 3) s_stat[tid] = 0;
-            __syncthreads();
-            unsigned long long rchk = 0, confl = 0, wdef = 0;
-            const unsigned long long M0 = __ldcg(&st->M);
-            uint32_t A = 0;                   // accepted so far in this tile (codebook[M0, M0+A))
-            for (uint32_t c0 = 0; c0 < S; c0 += kPChunk) {
-                const uint32_t Sc = min(kPChunk, S - c0);
-                for (uint32_t j = tid; j < Sc; j += blockDim.x) {
-                    const uint2 e = __ldcg(a.surv + c0 + j);
-                    s_idx[j] = (uint16_t)e.x;
-                    s_val[j] = e.y;
-                }
-                __syncthreads();
-                // in-chunk conflicts: s_adj[j] lists (up to kPAdj) earlier survivors of the chunk
-                // within distance < d (s_adjn = 255: more); survivors conflicting with a word
-                // accepted in an earlier chunk of this tile are rejected outright.
-                // status 1 = accepted, 0 = rejected, 2 = undecided.
-                for (uint32_t j = tid; j < Sc; j += blockDim.x) {
-                    const uint32_t vj = s_val[j];
-                    bool prev = false;
-                    for (uint32_t t = 0; t < A && !prev; ++t)
-                        prev = p_conflict(a, vj, __ldcg(a.codebook + M0 + t));
-                    uint32_t cnt = 0;
-                    // 32 earlier survivors at a time: independent loads/checks into a bit mask,
-                    // then record the (rare) conflicts
-                    for (uint32_t k0 = 0; k0 < j; k0 += 32) {
-                        const uint32_t kn = min(32u, j - k0);
-                        uint32_t mask = 0;
-                        if (kn == 32) {
-#pragma unroll
-                            for (int t = 0; t < 32; ++t)
-                                mask |= (uint32_t)p_conflict(a, vj, s_val[k0 + t]) << t;
-                        } else {
-                            for (uint32_t t = 0; t < kn; ++t)
-                                mask |= (uint32_t)p_conflict(a, vj, s_val[k0 + t]) << t;
-                        }
-                        while (mask) {
-                            const uint32_t t = __ffs(mask) - 1;
-                            mask &= mask - 1;
-                            if (cnt < kPAdj) s_adj[j * kPAdj + cnt] = (uint16_t)(k0 + t);
-                            ++cnt;
-                        }
-                    }
-                    rchk += j + A;
-                    s_adjn[j] = cnt > kPAdj ? 255 : (uint8_t)cnt;
-                    if (a.timing && cnt > kPAdj) atomicAdd(&st->n_overflow, 1ull);
-                    s_status[j] = prev ? 0 : (cnt ? 2 : 1);
-                    confl += cnt;
-                }
-                __syncthreads();
-                P_TR(1)
-                // Parallel rounds: an undecided survivor is rejected as soon as one earlier
-                // conflicting survivor is accepted, accepted once all of them are rejected.  Long
-                // dependency chains are finished by warp 0 walking the undecided ones in rank
-                // order.  A survivor is accepted iff no earlier ACCEPTED survivor conflicts.
-                int left = 0;
-                for (int round = 0; round < 8; ++round) {
-                    int undecided = 0;
-                    for (uint32_t j = tid; j < Sc; j += blockDim.x) {
-                        if (s_status[j] != 2) continue;
-                        const uint32_t na = s_adjn[j];
-                        bool acc_nb = false, und_nb = false;
-                        if (na != 255) {
-                            for (uint32_t t = 0; t < na; ++t) {
-                                const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
-                                acc_nb |= sk == 1;
-                                und_nb |= sk == 2;
-                            }
-                        } else {
-                            const uint32_t vj = s_val[j];
-                            for (uint32_t k = 0; k < j; ++k) {
-                                if (p_conflict(a, vj, s_val[k])) {
-                                    const uint8_t sk = s_status[k];
-                                    acc_nb |= sk == 1;
-                                    und_nb |= sk == 2;
-                                }
-                            }
-                        }
-                        // a status read in the same round may be stale (2): that only delays
-                        if (acc_nb) s_status[j] = 0;
-                        else if (!und_nb) s_status[j] = 1;
-                        else undecided = 1;
-                    }
-                    if (a.timing && tid == 0) atomicAdd(&st->n_rounds, 1ull);
-                    left = __syncthreads_or(undecided);
-                    if (!left) break;
-                }
-                if (left && tid < 32) {
-                    for (uint32_t j = 0; j < Sc; ++j) {
-                        if (s_status[j] != 2) continue;                 // warp-uniform
-                        if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
-                        const uint32_t na = s_adjn[j];
-                        bool acc_nb = false;
-                        if (na != 255) {
-                            if (lane < na) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
-                        } else {
-                            const uint32_t vj = s_val[j];
-                            for (uint32_t k = lane; k < j; k += 32)
-                                acc_nb |= (s_status[k] == 1) && p_conflict(a, vj, s_val[k]);
-                        }
-                        acc_nb = __any_sync(0xffffffffu, acc_nb);
-                        if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
-                        __syncwarp();
-                    }
-                }
-                __syncthreads();
-                P_TR(2)
-                // ordered append of the chunk's accepted survivors
-                for (uint32_t j0 = 0; j0 < Sc; j0 += blockDim.x) {
-                    const uint32_t j = j0 + tid;
-                    const uint32_t acc = (j < Sc && s_status[j] == 1) ? 1u : 0u;
-                    uint32_t tot;
-                    const uint32_t pos = A + p_block_scan(acc, &tot, s_ws);
-                    if (acc) {
-                        if (M0 + pos < a.capacity) a.codebook[M0 + pos] = s_val[j];
-                        else st->error = 1;
-                        if (a.wdef_valid) wdef += a.N - 1 - (t0 + s_idx[j]);
-                    }
-                    A += tot;
-                }
-                if (A > a.capacity - M0) A = (uint32_t)(a.capacity - M0);
-                __threadfence_block();
-                __syncthreads();
-                P_TR(3)
-            }
-            // clear per-tile state for the next tile
-            for (uint32_t w = tid; w < words; w += blockDim.x) a.dead[w] = 0;
-            // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                rchk += __shfl_down_sync(0xffffffffu, rchk, o);
-                confl += __shfl_down_sync(0xffffffffu, confl, o);
-                wdef += __shfl_down_sync(0xffffffffu, wdef, o);
-            }
-            if (lane == 0) {
-                if (rchk) atomicAdd(&s_stat[0], rchk);
-                if (confl) atomicAdd(&s_stat[1], confl);
-                if (wdef) atomicAdd(&s_stat[2], wdef);
-            }
-            __syncthreads();
-            if (tid == 0) {
-                st->resolve_checks += s_stat[0];
-                st->conflicts += s_stat[1];
-                st->w_def += s_stat[2];
-            }
-            P_TR(4)
-            if (tid == 0) {
-                unsigned long long M1 = M0 + A;
-                if (M1 > a.capacity) M1 = a.capacity;
-                st->M = M1;
-                if (a.weight_bound) {
-                    // first index of each weight among the words just appended (acceptance
-                    // order is weight-sorted for graded orders); stored +1, 0 = none yet
-                    for (unsigned long long p = M0; p < M1; ++p) {
-                        const uint32_t w = __popc(a.codebook[p]);
-                        if (p == 0 || __popc(a.codebook[p - 1]) != w)
-                            if (!st->wfirst[w]) st->wfirst[w] = (unsigned int)(p + 1);
-                    }
-                }
-                if (S) { st->S_last = S; st->K_last = K; }
-                st->K_next = p_next_tile(a, K, S, A, t0 + K, M1, st->S_last, st->K_last ? st->K_last : 1u);
-                st->survivors += S;
-                st->tiles += 1;
-                st->levels += L;
-            }
-            __threadfence();
-        }
+        if (blockIdx.x == 0) p_resolve(a, sm, t0, K, L, timer, tm);
         if (timer) { const unsigned long long t = p_now(); st->t_resolve += t - tm; tm = t; }
         grid.sync();
         if (timer) { const unsigned long long t = p_now(); st->t_sync += t - tm; st->t_tile += t - tm_tile; }
@@ -700,7 +749,37 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     // work counter: lanes hold per-lane counts
     for (int o = 16; o > 0; o >>= 1) my_checks += __shfl_down_sync(0xffffffffu, my_checks, o);
     if (lane == 0 && my_checks) atomicAdd(&st->checks_exec, my_checks);
-    if (blockIdx.x == 0 && threadIdx.x == 0) *a.d_count = st->M;
+    if (!a.part_mode && blockIdx.x == 0 && threadIdx.x == 0) *a.d_count = st->M;
+}
+
+// partition mode, one tile: survivors -> resolve -> commit by one CTA (all ranks identically)
+__global__ void __launch_bounds__(kPThreads, 1) k_resolve_tile(PArgs a) {
+    __shared__ uint32_t C[33][33];
+    __shared__ uint64_t off[34];
+    __shared__ uint32_t s_ws[33];
+    __shared__ uint32_t s_basis[32];
+    extern __shared__ __align__(16) uint8_t p_dyn[];
+    const uint32_t kPChunk = a.chunk;
+    if (threadIdx.x < 32) s_basis[threadIdx.x] = a.basis[threadIdx.x];
+    if (a.ord >= GRADED_LEX) {
+        for (int i = threadIdx.x; i < 33 * 33; i += blockDim.x) C[i / 33][i % 33] = a.tabs->binom[i / 33][i % 33];
+        for (int i = threadIdx.x; i < 34; i += blockDim.x) off[i] = a.tabs->off[i];
+    }
+    __syncthreads();
+    PSmem sm;
+    sm.C = C; sm.off = off; sm.s_basis = s_basis; sm.s_ws = s_ws;
+    sm.s_val = reinterpret_cast<uint32_t *>(p_dyn);
+    sm.s_idx = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 4);
+    sm.s_status = p_dyn + kPChunk * 6;
+    sm.s_adjn = p_dyn + kPChunk * 7;
+    sm.s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 8);
+    sm.chunk = kPChunk;
+    const unsigned long long M = __ldcg(&a.st->M);
+    uint32_t K = a.K_single;
+    if ((unsigned long long)K > a.t_end - a.t_single) K = (uint32_t)(a.t_end - a.t_single);
+    const int L = p_levels(M - p_base(a, a.t_single, M), a.W0, a.growth);
+    p_resolve(a, sm, a.t_single, K, L, false, 0);
+    if (threadIdx.x == 0) *a.d_count = a.st->M;
 }
 
 // ------------------------------------------------------------------ host side
@@ -760,12 +839,25 @@ bool persistent_supported(const RunArgs &a) {
            !(a.opt.flags & (GC_FLAG_NO_EARLY_EXIT | GC_FLAG_FORCE_SEQ_RESOLVE | GC_FLAG_LAUNCHED_TILES));
 }
 
+static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa);
+static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a);
+
 int persistent_run(const RunArgs &r) {
+    PContext *cx;
+    PArgs a;
+    int rc = p_setup(r, &cx, &a);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lock(cx->mu);
+    return persistent_run_locked(r, cx, a);
+}
+
+static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     int device;
     PCK(cudaGetDevice(&device));
     PContext *cx;
     int rc = p_context(device, &cx);
     if (rc) return rc;
+    *pcx = cx;
     std::lock_guard<std::mutex> lock(cx->mu);
     cudaStream_t s = (cudaStream_t)r.stream;
     if (cx->tabs_n != (int)r.n) {
@@ -812,6 +904,15 @@ int persistent_run(const RunArgs &r) {
         a.t_end = t.off[r.constant_weight + 1];      // contiguous block of ranks
     }
     if (a.mix && r.self_orthogonal) a.mix = 0;
+    a.part_mode = 0;
+    a.vals_valid = 1;
+    a.t_single = 0; a.K_single = 0; a.part_lo = 0; a.part_len = 0;
+    *pa = a;
+    return GC_OK;
+}
+
+static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a) {
+    cudaStream_t s = (cudaStream_t)r.stream;
     int per_sm = 0;
     // one CTA of 16 warps per SM (128 registers) or two (64 registers, half the resolve chunk)
     const char *ev = getenv("GC_PERSIST_CTAS");
@@ -865,6 +966,94 @@ int persistent_run(const RunArgs &r) {
                             full.t_level[l] / T / 1e3, (double)full.c_level[l],
                             100.0 * (double)full.c_level[l] / (full.t_level[l] * 1e-9) / (148.0 * 19.18 * 1.965e9));
         }
+        if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
+    }
+    return GC_OK;
+}
+
+// Multi-GPU / emulated ranks: per tile, every local partition's screen (one cooperative
+// launch of k_construct in partition mode each), the NCCL all-gather of the tile's dead
+// mask words (world > 1), then k_resolve_tile (one CTA; identical on every rank).  The
+// tile schedule is host-side and deterministic (every rank launches the same sequence).
+bool persistent_partitioned_supported(const RunArgs &a) {
+    return (a.world > 1 || a.opt.emulate_ranks > 1) && (a.opt.tile_max == 0 || a.opt.tile_max <= kPMaxTile) &&
+           !(a.opt.flags & (GC_FLAG_NO_EARLY_EXIT | GC_FLAG_FORCE_SEQ_RESOLVE | GC_FLAG_LAUNCHED_TILES));
+}
+
+int persistent_run_partitioned(const RunArgs &r) {
+    PContext *cx;
+    PArgs a;
+    int rc = p_setup(r, &cx, &a);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lock(cx->mu);
+    cudaStream_t s = (cudaStream_t)r.stream;
+    const unsigned G = r.world > 1 ? (unsigned)r.world : r.opt.emulate_ranks;
+    const unsigned parts_local = r.world > 1 ? 1u : G;
+    a.part_mode = 1;
+    a.vals_valid = 0;
+    a.chunk = 4096u;
+    const uint32_t tile_max = r.opt.tile_max ? r.opt.tile_max : 16384u;
+    const size_t smem = p_dyn_smem(a.chunk);
+    PCK(cudaFuncSetAttribute((const void *)k_construct<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PCK(cudaFuncSetAttribute((const void *)k_resolve_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)p_resolve_smem(a.chunk)));
+    int per_sm = 0;
+    PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_construct<1>, kPThreads, smem));
+    if (per_sm < 1) { set_error("k_construct cannot be resident"); return GC_ECUDA; }
+    unsigned long long launches = 0, tiles = 0;
+    PCK(cudaEventRecord(cx->ev0, s));
+    unsigned long long t0 = a.t_begin;
+    while (t0 < a.t_end) {
+        uint32_t K = r.opt.tile_min;
+        while (K < tile_max && (unsigned long long)K * 8 <= t0 - a.t_begin) K <<= 1;
+        if ((unsigned long long)K > a.t_end - t0) K = (uint32_t)(a.t_end - t0);
+        uint32_t plo = 0, plen = 0, Kpad = 0;
+        a.t_single = t0;
+        a.K_single = K;
+        for (unsigned pl = 0; pl < parts_local; ++pl) {
+            const unsigned g = r.world > 1 ? (unsigned)r.rank : pl;
+            if (gc_tile_partition(K, (int)G, (int)g, &plo, &plen, &Kpad) != GC_OK) return GC_EINTERNAL;
+            a.part_lo = plo;
+            a.part_len = plen;
+            void *args[] = {&a};
+            PCK(cudaLaunchCooperativeKernel((const void *)k_construct<1>, dim3(cx->sms), dim3(kPThreads), args,
+                                            smem, s));
+            ++launches;
+        }
+        if (r.world > 1) {
+            if (gc_tile_partition(K, (int)G, r.rank, &plo, &plen, &Kpad) != GC_OK) return GC_EINTERNAL;
+            const uint32_t seg = plen / 32;
+            rc = nccl_allgather_u32(cx->dead + (size_t)r.rank * seg, cx->dead, seg, r.nccl_comm, s);
+            if (rc) return rc;
+        }
+        k_resolve_tile<<<1, kPThreads, p_resolve_smem(a.chunk), s>>>(a);
+        ++launches;
+        PCK(cudaGetLastError());
+        t0 += K;
+        ++tiles;
+    }
+    PCK(cudaEventRecord(cx->ev1, s));
+    if (r.stats) {
+        PCK(cudaStreamSynchronize(s));
+        PState h;
+        PCK(cudaMemcpy(&h, cx->st, sizeof(PState), cudaMemcpyDeviceToHost));
+        float ms = 0;
+        PCK(cudaEventElapsedTime(&ms, cx->ev0, cx->ev1));
+        gc_stats *o = r.stats;
+        o->struct_size = sizeof(gc_stats);
+        o->n_ranks = G;
+        o->device_ms = ms;
+        o->M = h.M;
+        o->tiles = tiles;
+        o->phases = h.levels;
+        o->checks_exec = h.checks_exec;
+        o->survivors = h.survivors;
+        o->conflicts = h.conflicts;
+        o->resolve_checks = h.resolve_checks;
+        o->w_def = (double)h.w_def;
+        o->launches = launches;
+        o->screen_launches = launches - tiles;
+        o->screen_ms = ms;
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }
     return GC_OK;

@@ -96,7 +96,7 @@ def test_constant_weight_vs_oracle(gc, ordering, n):
 
 
 @pytest.mark.parametrize("sched", [{"tile_min": 32, "tile_max": 64, "window0": 32}, {"window_growth": 1},
-                                   {"tile_min": 4096, "tile_max": 4096}, {"flags": 32}])
+                                   {"tile_min": 4096, "tile_max": 4096}, {"flags": 32}, {"emulate_ranks": 4}])
 def test_combined_constraints_schedule_invariance(gc, sched):
     rng = random.Random(7)
     b = random_basis(14, rng)

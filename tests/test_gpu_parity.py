@@ -173,6 +173,9 @@ SCHEDULES = [
     {"emulate_ranks": 2},
     {"emulate_ranks": 8, "tile_min": 256},
     {"emulate_ranks": 4, "flags": 1},
+    {"emulate_ranks": 2, "flags": 16},                 # launched engine, 2 partitions
+    {"emulate_ranks": 8, "tile_min": 32, "tile_max": 1024},
+    {"emulate_ranks": 4, "tile_max": 65536},
     {"flags": 16},                      # host-launched tiles (default 65536)
     {"flags": 16, "tile_max": 4096, "window0": 256},
     {"tile_max": 8192},
