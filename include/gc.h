@@ -91,6 +91,11 @@ typedef struct gc_options {
 #define GC_FLAG_NO_WEIGHT_BOUND 0x40u /* graded orders: screen the whole codebook (default: stop at the
                                         first codeword of weight >= wt(candidate) - d + 1, since the
                                         codebook is weight-sorted and |wt(u)-wt(v)| <= dist(u,v))     */
+#define GC_FLAG_NO_BLOCK_BOUND 0x80u /* persistent engine: scan every codeword block of a window (default:
+                                        skip a block of 32 codewords when the bit-consensus bound
+                                        popc((AND_blk & ~OR_batch) | (AND_batch & ~OR_blk)) -- positions
+                                        where every codeword of the block differs from every live
+                                        candidate of the warp -- is already >= d; exact)            */
 #define GC_FLAG_KERNEL_TIMING  0x8u  /* bracket every screen launch with CUDA events on the launching
                                         stream; fills gc_stats.screen_ms (benchmarking)               */
 

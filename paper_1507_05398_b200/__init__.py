@@ -15,6 +15,7 @@ from ._binding import (  # noqa: F401
     GC_FLAG_KERNEL_TIMING,
     GC_FLAG_LAUNCHED_TILES,
     GC_FLAG_NO_EARLY_EXIT,
+    GC_FLAG_NO_BLOCK_BOUND,
     GC_FLAG_NO_WEIGHT_BOUND,
     GC_FLAG_POPC_ONLY,
     GC_FLAG_SYNC_TILES,

@@ -26,6 +26,7 @@ GC_FLAG_KERNEL_TIMING = 0x8
 GC_FLAG_LAUNCHED_TILES = 0x10
 GC_FLAG_POPC_ONLY = 0x20
 GC_FLAG_NO_WEIGHT_BOUND = 0x40
+GC_FLAG_NO_BLOCK_BOUND = 0x80
 
 _STATUS = {0: "GC_OK", 1: "GC_EINVAL", 2: "GC_ERANGE", 3: "GC_ENOSPC", 4: "GC_EUNSUPPORTED",
            5: "GC_ECUDA", 6: "GC_ENOMEM", 7: "GC_ENCCL", 8: "GC_EINTERNAL"}

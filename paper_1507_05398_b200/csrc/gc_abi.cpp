@@ -33,8 +33,8 @@ int resolve_options(const gc_options *opt, Options *out) {
         o.flags = opt->flags;
         if (opt->window_growth) o.growth = opt->window_growth;
     }
-    if (o.growth < 1 || o.growth > 4) {
-        set_error("window_growth must be in [1, 4]");
+    if (o.growth > 12) {          // 0 = engine default
+        set_error("window_growth must be in [1, 12]");
         return GC_EINVAL;
     }
     if (!is_pow2(o.tile_min) || o.tile_min < 32 || (o.tile_max && (!is_pow2(o.tile_max) || o.tile_max > (1u << 20) ||
@@ -52,7 +52,7 @@ int resolve_options(const gc_options *opt, Options *out) {
     }
     if (o.flags & ~(uint32_t)(GC_FLAG_NO_EARLY_EXIT | GC_FLAG_SYNC_TILES | GC_FLAG_FORCE_SEQ_RESOLVE |
                               GC_FLAG_KERNEL_TIMING | GC_FLAG_LAUNCHED_TILES | GC_FLAG_POPC_ONLY |
-                              GC_FLAG_NO_WEIGHT_BOUND)) {
+                              GC_FLAG_NO_WEIGHT_BOUND | GC_FLAG_NO_BLOCK_BOUND)) {
         set_error("unknown bits in gc_options.flags");
         return GC_EINVAL;
     }

@@ -594,7 +594,7 @@ int engine_run(const RunArgs &a) {
                 M_ub = std::min(M_ub, Mk + (t0 - tile_end[k]));
             }
         }
-        int P = early ? phases_for(M_ub, o.window0, o.growth) : 1;
+        int P = early ? phases_for(M_ub, o.window0, o.growth ? o.growth : 2u) : 1;
         if (t0 == 0) P = 0;            // empty codebook before the first tile
         else if (P < 1) P = 1;
 
@@ -612,7 +612,7 @@ int engine_run(const RunArgs &a) {
                     if ((rc = cx->timing_event(nev++, &ea)) || (rc = cx->timing_event(nev++, &eb))) return rc;
                     CK(cudaEventRecord(ea, st));
                 }
-                k_screen<<<screen_grid, kScreenThreads, 0, st>>>(p, P, o.window0, (int)o.growth, early, a.d_codebook, cx->vals,
+                k_screen<<<screen_grid, kScreenThreads, 0, st>>>(p, P, o.window0, (int)(o.growth ? o.growth : 2u), early, a.d_codebook, cx->vals,
                                                                 lin, cin, plo, part, cx->dead, cx->ctr, a.d);
                 if (timing) CK(cudaEventRecord(eb, st));
                 ++launches;

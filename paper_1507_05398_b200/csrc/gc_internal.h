@@ -21,7 +21,8 @@ struct Options {
     uint32_t window0 = 4096;
     uint32_t emulate_ranks = 1;
     uint32_t flags = 0;
-    uint32_t growth = 2;            // log2 window growth per level
+    uint32_t growth = 0;            // log2 window growth per level, 0 = engine default (launched
+                                    // engine 2; persistent engine 4 with the block bound, else 2)
 };
 int resolve_options(const gc_options *opt, Options *out);   // GC_OK / GC_EINVAL
 

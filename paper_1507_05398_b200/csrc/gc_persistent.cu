@@ -42,7 +42,7 @@ constexpr int kPMaxLevels = 32;
 constexpr uint32_t kPMaxTile = 1u << 16;    // largest tile (tile indices fit in 16 bits)
 // survivors resolved per chunk (shared memory): 4096 with one CTA per SM, 2048 with two
 constexpr uint32_t kPMaxBatches = kPMaxTile / 32;
-constexpr uint32_t kPTargetAccepted = 128;  // adaptive tiles grow up to ~2x this many accepted words
+constexpr uint32_t kPTargetAccepted = 256;  // adaptive tiles grow up to ~2x this many accepted words
 constexpr uint32_t kPMaxPredictedSurvivors = 1024;
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + s_adjn (1 B) + s_adj (2 B x kPAdj)
@@ -82,6 +82,8 @@ struct PArgs {
     uint32_t chunk;                 // survivors per resolve chunk
     int weight_bound;               // graded orders: stop the screen at the weight bound
     int items_per_warp;             // target work items per warp and level
+    uint32_t target_accepted;       // adaptive tiles grow toward ~this many accepted words per tile
+    uint32_t sub_max_bound;         // longest window sub-range per warp item with the block bound
     // partition mode (multi-GPU / emulated ranks): one tile's screen over one candidate range
     int part_mode;
     unsigned long long t_single;
@@ -94,6 +96,13 @@ struct PArgs {
     int cw;                         // constant weight (-1: none)
     unsigned long long t_begin, t_end;   // ranks scanned (graded + constant weight: one class)
     int wdef_valid;                 // W_def counts every rank: only without filters
+    // block bound: per aligned block of 32 codewords (and of 1024) the AND and the OR of its
+    // words; a warp skips a block when popc((AND_blk & ~OR_c) | (AND_c & ~OR_blk)) >= d for
+    // the AND/OR of its live candidates (GC_FLAG_NO_BLOCK_BOUND turns it off)
+    int bound;
+    uint32_t nmask;                 // 2^n - 1
+    uint32_t *bAnd, *bOr;           // [ceil(capacity / 32)]
+    uint32_t *sAnd, *sOr;           // [ceil(capacity / 1024)]
     uint32_t *codebook;
     unsigned long long capacity;
     const OrderTables *tabs;
@@ -118,7 +127,7 @@ struct PArgs {
 __device__ __forceinline__ uint32_t p_next_tile(const PArgs &a, uint32_t K, uint32_t S, uint32_t A,
                                                 unsigned long long t1, unsigned long long M1,
                                                 uint32_t S_last, uint32_t K_last) {
-    const unsigned long long want = M1 ? (unsigned long long)kPTargetAccepted * t1 / M1 : ~0ull;
+    const unsigned long long want = M1 ? (unsigned long long)a.target_accepted * t1 / M1 : ~0ull;
     uint32_t cap = a.tile_min;
     // survivors predicted from the last tile that had any (bursty orders, e.g. graded ones at
     // large d, have long empty stretches): keep them <= kPMaxPredictedSurvivors
@@ -134,9 +143,14 @@ __device__ __forceinline__ uint32_t p_next_tile(const PArgs &a, uint32_t K, uint
 }
 
 // newest-first depth covered by levels 0 .. l-1: W0 (1 + g + ... + g^(l-1)), g = 2^growth
+// (window sizes saturate at 2^40, far above any codebook)
+__device__ __forceinline__ unsigned long long p_window(uint32_t W0, int growth, int l) {
+    const int sh = growth * l;
+    return sh >= 40 ? (1ull << 40) : min((unsigned long long)W0 << sh, 1ull << 40);
+}
 __device__ __forceinline__ unsigned long long p_depth(uint32_t W0, int growth, int l) {
-    unsigned long long dsum = 0, w = W0;
-    for (int i = 0; i < l; ++i) { dsum += w; w <<= growth; }
+    unsigned long long dsum = 0;
+    for (int i = 0; i < l; ++i) dsum += p_window(W0, growth, i);
     return dsum;
 }
 
@@ -216,6 +230,107 @@ __device__ __forceinline__ uint32_t p_scan(const uint32_t *__restrict__ cb, long
         if (__all_sync(0xffffffffu, done)) break;
         cur = nxt;
         top = ntop;
+    }
+    return scanned;
+}
+
+// Block bound (exact): at a bit position where every codeword of a block has the value x and
+// every live candidate of the warp has 1 - x, every candidate-codeword pair differs, so
+//   dist(v, c) >= popc((AND_blk & ~OR_cand) | (AND_cand & ~OR_blk))   for all v, c.
+// A block whose bound is >= d cannot hold a codeword closer than d to any of the candidates.
+__device__ __forceinline__ uint32_t p_lb(uint32_t bA, uint32_t bO, uint32_t cA, uint32_t cO, uint32_t nmask) {
+    return (uint32_t)__popc(((bA & ~cO) | (cA & ~bO)) & nmask);
+}
+
+// checks of the lane's R candidates against the (nv <= 32) codewords held by lanes 0..nv-1
+template <int R, int MIX>
+__device__ __forceinline__ void p_block(uint32_t cur, int nv, const uint32_t (&v)[R], uint32_t (&m)[R]) {
+    if (nv == 32) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t c = __shfl_sync(0xffffffffu, cur, k);
+#pragma unroll
+            for (int r = 0; r < R; ++r) p_check<MIX>(m[r], v[r], c, r);
+        }
+    } else {
+        for (int k = 0; k < nv; ++k) {
+            const uint32_t c = __shfl_sync(0xffffffffu, cur, k);
+#pragma unroll
+            for (int r = 0; r < R; ++r) p_check<MIX>(m[r], v[r], c, r);
+        }
+    }
+}
+
+template <int R, int MIX>
+__device__ __forceinline__ bool p_all_dead(const uint32_t (&m)[R], uint32_t d) {
+    bool done = true;
+#pragma unroll
+    for (int r = 0; r < R; ++r) done &= p_dead<MIX>(m[r], d, r);
+    return __all_sync(0xffffffffu, done);
+}
+
+// Aligned blocks kb..kt (newest first) of the codeword range [r_lo, r_hi): lane t tests block
+// kt - t (32 blocks per round), the warp scans the blocks that pass, prefetching the next one.
+// The codewords of block kt are fetched speculatively with its bound.  Returns true once every
+// candidate of the warp is dead.
+template <int R, int MIX>
+__device__ __forceinline__ bool p_scan_blocks(const PArgs &a, long long r_lo, long long r_hi, uint32_t cA, uint32_t cO,
+                                              const uint32_t (&v)[R], uint32_t (&m)[R], uint32_t &scanned) {
+    const int lane = threadIdx.x & 31;
+    const long long kb = r_lo >> 5;
+    for (long long kt = (r_hi - 1) >> 5; kt >= kb; kt -= 32) {
+        const long long k = kt - lane;
+        auto blk_top = [&](long long q) { return min(r_hi, (q + 1) << 5); };
+        auto blk_bot = [&](long long q) { return max(r_lo, q << 5); };
+        auto load = [&](long long q) {
+            const long long i = blk_top(q) - 1 - lane;
+            return i >= blk_bot(q) ? __ldcg(a.codebook + i) : 0u;
+        };
+        uint32_t cur = load(kt);
+        bool pass = false;
+        if (k >= kb) pass = p_lb(__ldcg(a.bAnd + k), __ldcg(a.bOr + k), cA, cO, a.nmask) < a.d;
+        uint32_t mask = __ballot_sync(0xffffffffu, pass);
+        if (mask && !(mask & 1u)) cur = load(kt - (__ffs(mask) - 1));
+        while (mask) {
+            const int t = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const uint32_t nxt = mask ? load(kt - (__ffs(mask) - 1)) : 0u;
+            const long long q = kt - t;
+            const int nv = (int)(blk_top(q) - blk_bot(q));
+            p_block<R, MIX>(cur, nv, v, m);
+            scanned += (uint32_t)nv;
+            if (p_all_dead<R, MIX>(m, a.d)) return true;
+            cur = nxt;
+        }
+    }
+    return false;
+}
+
+// scan [lo, hi) newest first with the block bound: ranges up to 4096 codewords test their
+// blocks directly; longer ones first test aligned super-blocks of 1024 codewords, 32 per
+// round, and only then the blocks of the super-blocks that pass
+template <int R, int MIX>
+__device__ __forceinline__ uint32_t p_scan_bound(const PArgs &a, long long lo, long long hi, uint32_t cA, uint32_t cO,
+                                                 const uint32_t (&v)[R], uint32_t (&m)[R]) {
+    const int lane = threadIdx.x & 31;
+    uint32_t scanned = 0;
+    if (hi - lo <= 4096) {
+        p_scan_blocks<R, MIX>(a, lo, hi, cA, cO, v, m, scanned);
+        return scanned;
+    }
+    const long long sb_lo = lo >> 10;
+    for (long long sg = (hi - 1) >> 10; sg >= sb_lo; sg -= 32) {
+        const long long sb = sg - lane;
+        bool pass = false;
+        if (sb >= sb_lo) pass = p_lb(__ldcg(a.sAnd + sb), __ldcg(a.sOr + sb), cA, cO, a.nmask) < a.d;
+        uint32_t mask = __ballot_sync(0xffffffffu, pass);
+        while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const long long s = sg - j;
+            if (p_scan_blocks<R, MIX>(a, max(lo, s << 10), min(hi, (s + 1) << 10), cA, cO, v, m, scanned))
+                return scanned;
+        }
     }
     return scanned;
 }
@@ -308,7 +423,7 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
     const long long s_hi = lv.hi - (long long)j * lv.sub;            // j = 0: newest
     const long long s_lo = max(lv.lo, s_hi - lv.sub);
     // first codeword block in flight while the candidates are fetched
-    const uint32_t cur0 = (s_hi - 1 - lane >= s_lo) ? __ldcg(a.codebook + s_hi - 1 - lane) : 0u;
+    const uint32_t cur0 = (!a.bound || MIX == 1) && (s_hi - 1 - lane >= s_lo) ? __ldcg(a.codebook + s_hi - 1 - lane) : 0u;
     uint32_t v[R], m[R], idx[R];
     bool live[R], filtered[R];
 #pragma unroll
@@ -345,7 +460,18 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
     const bool scan = __any_sync(0xffffffffu, any);
     if (scan || __any_sync(0xffffffffu, any_filtered)) {
         if (scan) {
-            const uint32_t sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
+            uint32_t sc;
+            if (MIX != 1 && a.bound) {
+                // AND / OR of the warp's live candidates (identity for the others)
+                uint32_t la = ~0u, lo_ = 0u;
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+                    if (live[r]) { la &= v[r]; lo_ |= v[r]; }
+                const uint32_t cA = __reduce_and_sync(0xffffffffu, la), cO = __reduce_or_sync(0xffffffffu, lo_);
+                sc = p_scan_bound<R, MIX>(a, s_lo, s_hi, cA, cO, v, m);
+            } else {
+                sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
+            }
             my_checks += (unsigned long long)sc * R;   // per lane; summed over lanes at the end
         }
 #pragma unroll
@@ -564,6 +690,25 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
             __syncthreads();
             P_TR(3)
         }
+        // block-bound summaries of the words appended at [M0, M0 + A): AND / OR per block of 32
+        // and per super-block of 1024 (appends only ever narrow the AND and widen the OR)
+        if (a.bound && A) {
+            // thread t holds position (M0 & ~31) + t: warp w covers aligned block (M0 >> 5) + w
+            const unsigned long long e = M0 + A, p0 = M0 & ~31ull;
+            for (unsigned long long p = p0 + tid; p < ((e + 31) & ~31ull); p += blockDim.x) {
+                const bool in = p >= M0 && p < e;
+                const uint32_t w = in ? __ldcg(a.codebook + p) : 0u;
+                const uint32_t an = __reduce_and_sync(0xffffffffu, in ? w : ~0u);
+                const uint32_t orr = __reduce_or_sync(0xffffffffu, w);
+                if (lane == 0) {
+                    const unsigned long long k = p >> 5;
+                    atomicAnd(a.bAnd + k, an);
+                    atomicOr(a.bOr + k, orr);
+                    atomicAnd(a.sAnd + (k >> 5), an);
+                    atomicOr(a.sOr + (k >> 5), orr);
+                }
+            }
+        }
         // clear per-tile state for the next tile
         for (uint32_t w = tid; w < words; w += blockDim.x) a.dead[w] = 0;
         // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
@@ -665,7 +810,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             // window of level l (newest-first positions), last level reaches 0
             const long long bp = (long long)p_depth(W0, a.growth, l);
             const long long hi = (long long)M - bp;
-            long long lo = (l == L - 1) ? (long long)base : hi - ((long long)W0 << (a.growth * l));
+            long long lo = (l == L - 1) ? (long long)base : hi - (long long)p_window(W0, a.growth, l);
             if (lo < (long long)base) lo = (long long)base;
             // live candidates of this level: level 0 all K; deeper levels from the dead mask,
             // compacted through a per-CTA prefix over the mask words (every CTA builds it)
@@ -705,7 +850,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                 sub = (wlen + want - 1) / want;
                 sub = (sub + 31) & ~31ll;
                 sub = max(sub, (long long)kPSubMin);
-                sub = min(sub, (long long)kPSubMax);
+                sub = min(sub, a.bound ? (long long)a.sub_max_bound : (long long)kPSubMax);
                 nsub = (uint32_t)((wlen + sub - 1) / sub);
             }
             const unsigned long long checks_before = my_checks;
@@ -789,6 +934,8 @@ struct PContext {
     uint32_t *vals = nullptr, *dead = nullptr;
     uint2 *q0 = nullptr, *q1 = nullptr, *surv = nullptr;
     uint8_t *status = nullptr;
+    uint32_t *bsum = nullptr;       // block-bound summaries: bAnd | bOr | sAnd | sOr
+    size_t bsum_words = 0;          // allocated u32 words
     PState *st = nullptr;
     OrderTables *tabs = nullptr;
     int tabs_n = -1;
@@ -873,20 +1020,46 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
         PCK(cudaStreamSynchronize(s));   // k0 lives on this stack frame
     }
     PCK(cudaMemsetAsync(cx->dead, 0, kPMaxTile / 8, s));
+    // block-bound summaries for the whole capacity (AND = all ones, OR = 0 before any append)
+    const size_t nblk = (size_t)((r.capacity + 31) / 32) + 1, nsup = (size_t)((r.capacity + 1023) / 1024) + 1;
+    const size_t need = 2 * (nblk + nsup);
+    if (cx->bsum_words < need) {
+        if (cx->bsum) PCK(cudaFree(cx->bsum));
+        cx->bsum = nullptr;
+        cx->bsum_words = 0;
+        PCK(cudaMalloc(&cx->bsum, need * 4));
+        cx->bsum_words = need;
+    }
+    PCK(cudaMemsetAsync(cx->bsum, 0xff, nblk * 4, s));
+    PCK(cudaMemsetAsync(cx->bsum + nblk, 0, nblk * 4, s));
+    PCK(cudaMemsetAsync(cx->bsum + 2 * nblk, 0xff, nsup * 4, s));
+    PCK(cudaMemsetAsync(cx->bsum + 2 * nblk + nsup, 0, nsup * 4, s));
     PArgs a;
+    a.bAnd = cx->bsum;
+    a.bOr = cx->bsum + nblk;
+    a.sAnd = cx->bsum + 2 * nblk;
+    a.sOr = cx->bsum + 2 * nblk + nsup;
+    a.nmask = r.n >= 32 ? 0xffffffffu : ((1u << r.n) - 1u);
     a.n = (int)r.n; a.ord = r.ordering; a.d = r.d;
     a.N = 1ull << r.n;
     a.tile_min = r.opt.tile_min; a.tile_max = r.opt.tile_max ? r.opt.tile_max : kPDefaultTile;
     if (a.tile_min > a.tile_max) a.tile_min = a.tile_max;
     a.W0 = r.opt.window0;
-    a.growth = (int)r.opt.growth;
+    a.growth = (int)(r.opt.growth ? r.opt.growth
+                                  : (!r.self_orthogonal && !(r.opt.flags & GC_FLAG_NO_BLOCK_BOUND)) ? 4u : 2u);
     a.mix = (r.d >= 2 && r.d <= 4 && !(r.opt.flags & GC_FLAG_POPC_ONLY)) ? (int)r.d : 0;
     a.codebook = r.d_codebook; a.capacity = r.capacity;
     a.tabs = cx->tabs; a.vals = cx->vals; a.dead = cx->dead;
     a.q0 = cx->q0; a.q1 = cx->q1; a.surv = cx->surv; a.status = cx->status;
     a.st = cx->st; a.d_count = (unsigned long long *)r.d_count;
     a.timing = getenv("GC_DEBUG_PHASES") != nullptr;
-    a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP"))) : 2;
+    a.bound = !r.self_orthogonal && !(r.opt.flags & GC_FLAG_NO_BLOCK_BOUND);
+    // with the block bound most of a window is skipped by summary tests: one item per warp and
+    // long sub-ranges keep a level to a few dependent round trips
+    a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP"))) : (a.bound ? 1 : 2);
+    a.sub_max_bound = getenv("GC_SUB_MAX") ? (uint32_t)std::max(64, atoi(getenv("GC_SUB_MAX"))) : 32768u;
+    a.target_accepted = getenv("GC_TARGET_ACCEPTED") ? (uint32_t)std::max(1, atoi(getenv("GC_TARGET_ACCEPTED")))
+                                                     : kPTargetAccepted;
     a.use_basis = r.use_basis;
     for (int i = 0; i < 32; ++i) a.basis[i] = r.basis[i];
     a.so = r.self_orthogonal;
@@ -925,7 +1098,9 @@ static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a) {
     if (per_sm < ctas) { set_error("k_construct cannot be resident"); return GC_ECUDA; }
     void *args[] = {&a};
     PCK(cudaEventRecord(cx->ev0, s));
-    PCK(cudaLaunchCooperativeKernel(kfn, dim3(cx->sms * ctas), dim3(kPThreads), args, smem, s));
+    int grid = cx->sms * ctas;
+    if (getenv("GC_GRID")) grid = std::max(1, std::min(grid, atoi(getenv("GC_GRID"))));
+    PCK(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kPThreads), args, smem, s));
     PCK(cudaEventRecord(cx->ev1, s));
     if (r.stats) {
         PCK(cudaStreamSynchronize(s));

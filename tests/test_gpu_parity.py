@@ -186,6 +186,8 @@ SCHEDULES = [
     {"window_growth": 1},
     {"flags": 32},                      # POPC only (no ALU-form checks)
     {"flags": 64},                      # no weight bound (graded orders screen everything)
+    {"flags": 128},                     # no block bound (every block of a window scanned)
+    {"flags": 192, "window0": 256},     # neither bound
     {"window_growth": 4, "window0": 64},
     {"flags": 16, "window_growth": 3, "window0": 128},
 ]
