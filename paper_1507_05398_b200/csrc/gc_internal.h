@@ -22,7 +22,7 @@ struct Options {
     uint32_t emulate_ranks = 1;
     uint32_t flags = 0;
     uint32_t growth = 0;            // log2 window growth per level, 0 = engine default (launched
-                                    // engine 2; persistent engine 4 with the block bound, else 2)
+                                    // engine 2; persistent engine: see p_setup)
 };
 int resolve_options(const gc_options *opt, Options *out);   // GC_OK / GC_EINVAL
 

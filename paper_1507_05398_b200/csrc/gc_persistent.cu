@@ -45,11 +45,20 @@ constexpr uint32_t kPMaxBatches = kPMaxTile / 32;
 constexpr uint32_t kPTargetAccepted = 256;  // adaptive tiles grow up to ~2x this many accepted words
 constexpr uint32_t kPMaxPredictedSurvivors = 1024;
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
-// resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + s_adjn (1 B) + s_adj (2 B x kPAdj)
-__host__ __device__ constexpr size_t p_resolve_smem(uint32_t chunk) { return (size_t)chunk * (8 + 2 * kPAdj); }
+constexpr uint32_t kPStageWords = 32 * 32;      // per-warp stage: 32 blocks of 32 codewords (4 KiB)
+constexpr uint32_t kPWarpStage = kPStageWords + 8 * 64 + 32;   // + 8 super-blocks' block summaries + a block queue
+constexpr uint32_t kPOvf = 1024;                // overflow survivors decided warp-parallel (per chunk)
+constexpr uint32_t kPOvfMark = 0xffffffffu;     // s_cnt of a listed overflow survivor
+// resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + pad (1 B) + s_cnt (4 B) + s_adj (2 B x kPAdj)
+__host__ __device__ constexpr size_t p_resolve_smem(uint32_t chunk) { return (size_t)chunk * (12 + 2 * kPAdj); }
 // + level prefix: s_pre[kPMaxTile/32 + 1] and s_live[kPMaxTile/32]
+// the level stages (kPWarpStage words per warp) alias the resolve scratch: a CTA never runs both
+__host__ __device__ constexpr size_t p_scratch_smem(uint32_t chunk) {
+    return p_resolve_smem(chunk) > (size_t)kPWarps * kPWarpStage * 4 ? p_resolve_smem(chunk)
+                                                                      : (size_t)kPWarps * kPWarpStage * 4;
+}
 __host__ __device__ constexpr size_t p_dyn_smem(uint32_t chunk) {
-    return p_resolve_smem(chunk) + (size_t)(2 * (kPMaxTile / 32) + 4) * 4;
+    return p_scratch_smem(chunk) + (size_t)(2 * (kPMaxTile / 32) + 4) * 4;
 }
 
 struct PState {
@@ -65,9 +74,15 @@ struct PState {
     unsigned long long c_level[kPMaxLevels];   // diagnostics: lane-checks per level
     unsigned long long t_resolve, t_sync, t_tile;
     unsigned long long t_r[6];                 // resolve sub-steps
+    unsigned long long t_items[kPMaxLevels];   // diagnostics: level start -> last item done (any warp)
+    unsigned long long t_item_end[2];          // per-level scratch (alternating slots)
+    unsigned long long t_item_max[2];          // per-level scratch: longest warp item
+    unsigned long long t_item_sum[kPMaxLevels];
+    unsigned long long t_prefix[kPMaxLevels], n_live[kPMaxLevels], n_items[kPMaxLevels], t_itmax[kPMaxLevels];
     unsigned long long n_overflow, n_seq, n_rounds;
     unsigned int error;
     unsigned int K_next;                       // size of the next tile (set by CTA 0)
+    unsigned int item_ctr[kPMaxLevels];        // dynamic item claims per level (reset by the resolve)
     unsigned int S_last, K_last;               // last tile with survivors: its S and K
     unsigned int wfirst[33];                   // graded orders: 1 + index of the first codeword of weight w
 };
@@ -101,8 +116,8 @@ struct PArgs {
     // the AND/OR of its live candidates (GC_FLAG_NO_BLOCK_BOUND turns it off)
     int bound;
     uint32_t nmask;                 // 2^n - 1
-    uint32_t *bAnd, *bOr;           // [ceil(capacity / 32)]
-    uint32_t *sAnd, *sOr;           // [ceil(capacity / 1024)]
+    uint2 *bsum;                    // (AND, OR) per block of 32, [nblk] (multiple of 32)
+    uint2 *ssum;                    // (AND, OR) per super-block of 1024
     uint32_t *codebook;
     unsigned long long capacity;
     const OrderTables *tabs;
@@ -269,69 +284,195 @@ __device__ __forceinline__ bool p_all_dead(const uint32_t (&m)[R], uint32_t d) {
     return __all_sync(0xffffffffu, done);
 }
 
+// checks against the codewords stage[o_lo, o_hi) of one staged block (shared memory, the same
+// address in every lane: broadcast reads, four codewords per 128-bit load for a full block)
+template <int R, int MIX>
+__device__ __forceinline__ void p_block_smem(const uint32_t *stage, int o_lo, int o_hi, const uint32_t (&v)[R],
+                                             uint32_t (&m)[R]) {
+    if (o_lo == 0 && o_hi == 32) {
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(stage);
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+            const uint4 c = s4[k4];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                p_check<MIX>(m[r], v[r], c.x, r);
+                p_check<MIX>(m[r], v[r], c.y, r);
+                p_check<MIX>(m[r], v[r], c.z, r);
+                p_check<MIX>(m[r], v[r], c.w, r);
+            }
+        }
+    } else {
+        for (int k = o_lo; k < o_hi; ++k) {
+            const uint32_t c = stage[k];
+#pragma unroll
+            for (int r = 0; r < R; ++r) p_check<MIX>(m[r], v[r], c, r);
+        }
+    }
+}
+
+__device__ __forceinline__ void p_cp_async16(uint32_t *dst, const uint32_t *src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void p_cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+}
+
 // Aligned blocks kb..kt (newest first) of the codeword range [r_lo, r_hi): lane t tests block
-// kt - t (32 blocks per round), the warp scans the blocks that pass, prefetching the next one.
-// The codewords of block kt are fetched speculatively with its bound.  Returns true once every
-// candidate of the warp is dead.
+// kt - t (32 blocks per round).  The codewords of block kt are fetched into registers together
+// with the bounds (speculatively); every other passing block is copied at once into the warp's
+// shared-memory stage (cp.async, 16 B per lane, L2 only) while block kt is checked, so a round
+// costs two dependent round trips however many blocks pass.  Returns true once every candidate
+// of the warp is dead.
 template <int R, int MIX>
 __device__ __forceinline__ bool p_scan_blocks(const PArgs &a, long long r_lo, long long r_hi, uint32_t cA, uint32_t cO,
-                                              const uint32_t (&v)[R], uint32_t (&m)[R], uint32_t &scanned) {
+                                              const uint32_t (&v)[R], uint32_t (&m)[R], uint32_t &scanned,
+                                              uint32_t *stage) {
     const int lane = threadIdx.x & 31;
     const long long kb = r_lo >> 5;
     for (long long kt = (r_hi - 1) >> 5; kt >= kb; kt -= 32) {
         const long long k = kt - lane;
         auto blk_top = [&](long long q) { return min(r_hi, (q + 1) << 5); };
         auto blk_bot = [&](long long q) { return max(r_lo, q << 5); };
-        auto load = [&](long long q) {
-            const long long i = blk_top(q) - 1 - lane;
-            return i >= blk_bot(q) ? __ldcg(a.codebook + i) : 0u;
-        };
-        uint32_t cur = load(kt);
+        const long long i0 = blk_top(kt) - 1 - lane;
+        const uint32_t cur = i0 >= blk_bot(kt) ? __ldcg(a.codebook + i0) : 0u;
         bool pass = false;
-        if (k >= kb) pass = p_lb(__ldcg(a.bAnd + k), __ldcg(a.bOr + k), cA, cO, a.nmask) < a.d;
-        uint32_t mask = __ballot_sync(0xffffffffu, pass);
-        if (mask && !(mask & 1u)) cur = load(kt - (__ffs(mask) - 1));
-        while (mask) {
-            const int t = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const uint32_t nxt = mask ? load(kt - (__ffs(mask) - 1)) : 0u;
-            const long long q = kt - t;
-            const int nv = (int)(blk_top(q) - blk_bot(q));
+        if (k >= kb) {
+            const uint2 bs = __ldcg(a.bsum + k);
+            pass = p_lb(bs.x, bs.y, cA, cO, a.nmask) < a.d;
+        }
+        const uint32_t mask = __ballot_sync(0xffffffffu, pass);
+        if (!mask) continue;
+        const uint32_t rest = mask & ~1u;             // block kt (bit 0) is checked from registers
+        const int nst = __popc(rest);
+        // stage: slot s <- the s-th passing block after kt, 8 lanes x 16 B per block; a 16-byte
+        // chunk reaching past the codebook's capacity is read word by word instead
+        for (int p = lane; p < 8 * nst; p += 32) {
+            const int sl = p >> 3, c4 = (p & 7) * 4;
+            const long long q = kt - (long long)(__fns(rest, 0, sl + 1));
+            const unsigned long long w0 = (unsigned long long)(q << 5) + c4;
+            if (w0 + 4 <= a.capacity) {
+                p_cp_async16(stage + sl * 32 + c4, a.codebook + w0);
+            } else {
+                for (int e = 0; e < 4; ++e)
+                    if (w0 + e < a.capacity) stage[sl * 32 + c4 + e] = __ldcg(a.codebook + w0 + e);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        if (mask & 1u) {
+            const int nv = (int)(blk_top(kt) - blk_bot(kt));
             p_block<R, MIX>(cur, nv, v, m);
             scanned += (uint32_t)nv;
-            if (p_all_dead<R, MIX>(m, a.d)) return true;
-            cur = nxt;
+            if (p_all_dead<R, MIX>(m, a.d)) { p_cp_async_wait_all(); return true; }
         }
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncwarp();
+        uint32_t mm = rest;
+        for (int sl = 0; sl < nst; ++sl) {
+            const int t = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const long long q = kt - t;
+            const int o_lo = (int)(blk_bot(q) - (q << 5)), o_hi = (int)(blk_top(q) - (q << 5));
+            p_block_smem<R, MIX>(stage + sl * 32, o_lo, o_hi, v, m);
+            scanned += (uint32_t)(o_hi - o_lo);
+            if (p_all_dead<R, MIX>(m, a.d)) { __syncwarp(); return true; }
+        }
+        __syncwarp();      // the stage is rewritten by the next round
     }
     return false;
 }
 
-// scan [lo, hi) newest first with the block bound: ranges up to 4096 codewords test their
-// blocks directly; longer ones first test aligned super-blocks of 1024 codewords, 32 per
-// round, and only then the blocks of the super-blocks that pass
+// Check the warp's candidates against the listed blocks blist[0, nb) of [lo, hi): all of
+// them are copied into the stage at once (cp.async, 8 lanes x 16 B per block, L2 only), then
+// scanned in list order.  Returns true once every candidate of the warp is dead.
+template <int R, int MIX>
+__device__ __forceinline__ bool p_scan_list(const PArgs &a, long long lo, long long hi, const uint32_t *blist, int nb,
+                                            const uint32_t (&v)[R], uint32_t (&m)[R], uint32_t &scanned,
+                                            uint32_t *stage) {
+    const int lane = threadIdx.x & 31;
+    for (int p = lane; p < 8 * nb; p += 32) {
+        const int sl = p >> 3, c4 = (p & 7) * 4;
+        const unsigned long long w0 = ((unsigned long long)blist[sl] << 5) + c4;
+        if (w0 + 4 <= a.capacity) {
+            p_cp_async16(stage + sl * 32 + c4, a.codebook + w0);
+        } else {
+            for (int e = 0; e < 4; ++e)
+                if (w0 + e < a.capacity) stage[sl * 32 + c4 + e] = __ldcg(a.codebook + w0 + e);
+        }
+    }
+    p_cp_async_wait_all();
+    for (int sl = 0; sl < nb; ++sl) {
+        const long long q = blist[sl];
+        const int o_lo = (int)(max(lo, q << 5) - (q << 5)), o_hi = (int)(min(hi, (q + 1) << 5) - (q << 5));
+        p_block_smem<R, MIX>(stage + sl * 32, o_lo, o_hi, v, m);
+        scanned += (uint32_t)(o_hi - o_lo);
+        if (p_all_dead<R, MIX>(m, a.d)) { __syncwarp(); return true; }
+    }
+    __syncwarp();      // the stage and the list are rewritten next
+    return false;
+}
+
+// scan [lo, hi) newest first with the block bound.  Ranges up to 4096 codewords test their
+// blocks directly (p_scan_blocks).  Longer ones go down a hierarchy, newest first, with a
+// fixed number of dependent round trips per round whatever passes:
+//   1. lane j tests super-block sg - j (1024 codewords) from its (AND, OR) summary;
+//   2. the block summaries of up to 8 passing super-blocks are copied to shared memory at once
+//      (256 B each) and tested there, one block per lane;
+//   3. the passing blocks are queued; every 32 of them are staged and checked (p_scan_list).
 template <int R, int MIX>
 __device__ __forceinline__ uint32_t p_scan_bound(const PArgs &a, long long lo, long long hi, uint32_t cA, uint32_t cO,
-                                                 const uint32_t (&v)[R], uint32_t (&m)[R]) {
+                                                 const uint32_t (&v)[R], uint32_t (&m)[R], uint32_t *stage) {
     const int lane = threadIdx.x & 31;
     uint32_t scanned = 0;
     if (hi - lo <= 4096) {
-        p_scan_blocks<R, MIX>(a, lo, hi, cA, cO, v, m, scanned);
+        p_scan_blocks<R, MIX>(a, lo, hi, cA, cO, v, m, scanned, stage);
         return scanned;
     }
-    const long long sb_lo = lo >> 10;
+    uint32_t *sstage = stage + kPStageWords;                 // 8 super-blocks x 32 (AND, OR)
+    uint32_t *blist = sstage + 8 * 64;                       // 32 queued block indices
+    const long long sb_lo = lo >> 10, kb = lo >> 5, kt = (hi - 1) >> 5;
+    int nb = 0;
     for (long long sg = (hi - 1) >> 10; sg >= sb_lo; sg -= 32) {
         const long long sb = sg - lane;
         bool pass = false;
-        if (sb >= sb_lo) pass = p_lb(__ldcg(a.sAnd + sb), __ldcg(a.sOr + sb), cA, cO, a.nmask) < a.d;
-        uint32_t mask = __ballot_sync(0xffffffffu, pass);
-        while (mask) {
-            const int j = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const long long s = sg - j;
-            if (p_scan_blocks<R, MIX>(a, max(lo, s << 10), min(hi, (s + 1) << 10), cA, cO, v, m, scanned))
-                return scanned;
+        if (sb >= sb_lo) {
+            const uint2 ss = __ldcg(a.ssum + sb);
+            pass = p_lb(ss.x, ss.y, cA, cO, a.nmask) < a.d;
+        }
+        uint32_t smask = __ballot_sync(0xffffffffu, pass);
+        while (smask) {
+            const int ns = min(8, __popc(smask));
+            for (int p = lane; p < 16 * ns; p += 32) {
+                const int sl = p >> 4, c = p & 15;
+                const long long s = sg - (long long)__fns(smask, 0, sl + 1);
+                p_cp_async16(sstage + sl * 64 + c * 4, reinterpret_cast<const uint32_t *>(a.bsum + (s << 5)) + c * 4);
+            }
+            p_cp_async_wait_all();
+            for (int sl = 0; sl < ns; ++sl) {
+                const long long s = sg - (long long)(__ffs(smask) - 1);
+                smask &= smask - 1;
+                const long long k = (s << 5) + 31 - lane;            // newest block first
+                bool bp = false;
+                if (k >= kb && k <= kt) {
+                    const uint32_t *e = sstage + sl * 64 + 2 * (31 - lane);
+                    bp = p_lb(e[0], e[1], cA, cO, a.nmask) < a.d;
+                }
+                const uint32_t bm = __ballot_sync(0xffffffffu, bp);
+                if (!bm) continue;
+                if (nb + __popc(bm) > 32) {
+                    if (p_scan_list<R, MIX>(a, lo, hi, blist, nb, v, m, scanned, stage)) return scanned;
+                    nb = 0;
+                }
+                if (bp) blist[nb + __popc(bm & ((1u << lane) - 1u))] = (uint32_t)k;
+                nb += __popc(bm);
+                __syncwarp();
+            }
         }
     }
+    if (nb) p_scan_list<R, MIX>(a, lo, hi, blist, nb, v, m, scanned, stage);
     return scanned;
 }
 
@@ -394,6 +535,7 @@ struct PLevel {
     const uint32_t *s_live;  // level >= 1: live bits per mask word (smem)
     uint32_t words;
     const uint32_t *basis;   // B-ordering basis (smem)
+    uint32_t *stage;         // block-bound staging, kPStageWords per warp (smem; aliases the resolve scratch)
     uint32_t c_lo;           // first tile index of the screened range
     uint32_t w_base;         // 32 * (first mask word of the range)
 };
@@ -440,13 +582,18 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                 if (!p_allowed(a, v[r])) { filtered[r] = true; live[r] = false; }
             } else {
                 idx[r] = p_locate(lv, q);
-                v[r] = __ldcg(a.vals + idx[r]);
+                // lex / Gray / B-ordering: regenerate from the rank (a few ALU ops, no round
+                // trip); graded orders: load the value level 0 stored (unranking is O(n))
+                v[r] = a.ord < GRADED_LEX || a.use_basis ? p_gen(a, C, off, lv.basis, lv.t0 + idx[r])
+                                                         : __ldcg(a.vals + idx[r]);
             }
             // another sub-range of this level may already have killed it (load issued in
             // parallel with the value / codeword loads)
             // (level 0 only: deeper levels hold mostly true survivors, and the load would sit
             // on their critical path)
-            if (lv.l == 0 && lv.nsub > 1 && live[r])
+            // (not with the block bound: level-0 items all run at once, the bit is rarely set
+            // yet, and the load would delay the bound tests by a round trip)
+            if (lv.l == 0 && lv.nsub > 1 && live[r] && (!a.bound || MIX == 1))
                 live[r] = !((__ldcg(a.dead + (idx[r] >> 5)) >> (idx[r] & 31)) & 1u);
         }
         m[r] = live[r] ? 0xffffffffu : 0u;      // dead lanes start "already dead" in both forms
@@ -468,7 +615,7 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                 for (int r = 0; r < R; ++r)
                     if (live[r]) { la &= v[r]; lo_ |= v[r]; }
                 const uint32_t cA = __reduce_and_sync(0xffffffffu, la), cO = __reduce_or_sync(0xffffffffu, lo_);
-                sc = p_scan_bound<R, MIX>(a, s_lo, s_hi, cA, cO, v, m);
+                sc = p_scan_bound<R, MIX>(a, s_lo, s_hi, cA, cO, v, m, lv.stage + (threadIdx.x >> 5) * kPWarpStage);
             } else {
                 sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
             }
@@ -508,249 +655,308 @@ __device__ __forceinline__ unsigned long long p_base(const PArgs &a, unsigned lo
     return M;
 }
 
+// diagnostics (GC_DEBUG_PHASES): accumulated by thread 0 of CTA 0 in local memory, written once
+struct PTimers {
+    unsigned long long level[kPMaxLevels], items[kPMaxLevels];
+    unsigned long long prefix[kPMaxLevels], live[kPMaxLevels], items_n[kPMaxLevels], item_max[kPMaxLevels];
+    unsigned long long resolve, sync, tile, r[6];
+};
+
 struct PSmem {
     const uint32_t (*C)[33];
     const uint64_t *off;
     const uint32_t *s_basis;
     uint32_t *s_ws, *s_val;
     uint16_t *s_idx;
-    uint8_t *s_status, *s_adjn;
+    uint8_t *s_status;
+    uint32_t *s_cnt;
     uint16_t *s_adj;
     uint32_t chunk;
 };
 
 __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsigned long long t0, uint32_t K, int L,
-                                       bool timer, unsigned long long tm) {
+                                          PTimers *timer, unsigned long long tm) {
     const uint32_t kPChunk = sm.chunk;
     const uint32_t (*C)[33] = sm.C;
     const uint64_t *off = sm.off;
     const uint32_t *s_basis = sm.s_basis;
-    uint32_t *s_ws = sm.s_ws, *s_val = sm.s_val;
+    uint32_t *s_ws = sm.s_ws, *s_val = sm.s_val, *s_cnt = sm.s_cnt;
     uint16_t *s_idx = sm.s_idx;
-    uint8_t *s_status = sm.s_status, *s_adjn = sm.s_adjn;
+    uint8_t *s_status = sm.s_status;
     uint16_t *s_adj = sm.s_adj;
     PState *st = a.st;
     const int lane = threadIdx.x & 31;
     const uint32_t words = (K + 31) / 32;
-        const uint32_t tid = threadIdx.x;
-        if (L == 0) {      // empty codebook: no level generated the candidates
-            for (uint32_t i = tid; i < K; i += blockDim.x) {
-                const uint32_t v = p_gen(a, C, off, s_basis, t0 + i);
-                a.vals[i] = v;
-                if (!p_allowed(a, v)) atomicOr(&a.dead[i >> 5], 1u << (i & 31));
-            }
-            __syncthreads();
-        }
-        // survivors in rank order -> a.surv (global; S <= K)
-        uint32_t S = 0;
-        for (uint32_t w0 = 0; w0 < words; w0 += blockDim.x) {
-            const uint32_t w = w0 + tid;
-            uint32_t alive = 0;
-            if (w < words) {
-                alive = ~__ldcg(a.dead + w);
-                if (w * 32 + 32 > K) alive &= (1u << (K - w * 32)) - 1u;
-            }
-            uint32_t tot;
-            uint32_t pos = S + p_block_scan(__popc(alive), &tot, s_ws);
-            while (alive) {
-                const int bit = __ffs(alive) - 1;
-                alive &= alive - 1;
-                const uint32_t i = w * 32 + bit;
-                a.surv[pos++] = make_uint2(i, a.vals_valid ? __ldcg(a.vals + i) : p_gen(a, C, off, s_basis, t0 + i));
-            }
-            S += tot;
-        }
+    const uint32_t tid = threadIdx.x;
+    if (L == 0) {      // empty codebook: no level ran, so the filters are applied here
+        for (uint32_t i = tid; i < K; i += blockDim.x)
+            if (!p_allowed(a, p_gen(a, C, off, s_basis, t0 + i))) atomicOr(&a.dead[i >> 5], 1u << (i & 31));
         __syncthreads();
-        unsigned long long tr = timer ? p_now() : 0;
-#define P_TR(i) if (timer) { const unsigned long long t_ = p_now(); st->t_r[i] += t_ - tr; tr = t_; }
-        if (timer) st->t_r[0] += tr - tm;
-        __shared__ unsigned long long s_stat[3];
-        if (tid < 3) s_stat[tid] = 0;
-        __syncthreads();
-        unsigned long long rchk = 0, confl = 0, wdef = 0;
-        const unsigned long long M0 = __ldcg(&st->M);
-        uint32_t A = 0;                   // accepted so far in this tile (codebook[M0, M0+A))
-        for (uint32_t c0 = 0; c0 < S; c0 += kPChunk) {
-            const uint32_t Sc = min(kPChunk, S - c0);
+    }
+    // a3.1 survivors in rank order, values regenerated from their ranks (no load): the first
+    // chunk straight into shared memory, any further ones to a.surv (S <= K)
+    uint32_t S = 0;
+    for (uint32_t w0 = 0; w0 < words; w0 += blockDim.x) {
+        const uint32_t w = w0 + tid;
+        uint32_t alive = 0;
+        if (w < words) {
+            alive = ~__ldcg(a.dead + w);
+            if (w * 32 + 32 > K) alive &= (1u << (K - w * 32)) - 1u;
+        }
+        uint32_t tot;
+        uint32_t pos = S + p_block_scan(__popc(alive), &tot, s_ws);
+        while (alive) {
+            const int bit = __ffs(alive) - 1;
+            alive &= alive - 1;
+            const uint32_t i = w * 32 + bit;
+            const uint32_t v = p_gen(a, C, off, s_basis, t0 + i);
+            if (pos < kPChunk) { s_idx[pos] = (uint16_t)i; s_val[pos] = v; }
+            else a.surv[pos] = make_uint2(i, v);
+            ++pos;
+        }
+        S += tot;
+    }
+    __syncthreads();
+    unsigned long long tr = timer ? p_now() : 0;
+#define P_TR(i) if (timer) { const unsigned long long t_ = p_now(); timer->r[i] += t_ - tr; tr = t_; }
+    if (timer) timer->r[0] += tr - tm;
+    __shared__ unsigned long long s_stat[3];
+    __shared__ uint16_t s_ovf[kPOvf];
+    __shared__ uint32_t s_novf;
+    if (tid < 3) s_stat[tid] = 0;
+    unsigned long long rchk = 0, confl = 0, wdef = 0;
+    const unsigned long long M0 = __ldcg(&st->M);
+    uint32_t A = 0;                   // accepted so far in this tile (codebook[M0, M0+A))
+    for (uint32_t c0 = 0; c0 < S; c0 += kPChunk) {
+        const uint32_t Sc = min(kPChunk, S - c0);
+        if (c0 > 0) {
             for (uint32_t j = tid; j < Sc; j += blockDim.x) {
                 const uint2 e = __ldcg(a.surv + c0 + j);
                 s_idx[j] = (uint16_t)e.x;
                 s_val[j] = e.y;
             }
-            __syncthreads();
-            // in-chunk conflicts: s_adj[j] lists (up to kPAdj) earlier survivors of the chunk
-            // within distance < d (s_adjn = 255: more); survivors conflicting with a word
-            // accepted in an earlier chunk of this tile are rejected outright.
-            // status 1 = accepted, 0 = rejected, 2 = undecided.
-            for (uint32_t j = tid; j < Sc; j += blockDim.x) {
-                const uint32_t vj = s_val[j];
-                bool prev = false;
-                for (uint32_t t = 0; t < A && !prev; ++t)
-                    prev = p_conflict(a, vj, __ldcg(a.codebook + M0 + t));
-                uint32_t cnt = 0;
-                // 32 earlier survivors at a time: independent loads/checks into a bit mask,
-                // then record the (rare) conflicts
-                for (uint32_t k0 = 0; k0 < j; k0 += 32) {
-                    const uint32_t kn = min(32u, j - k0);
-                    uint32_t mask = 0;
-                    if (kn == 32) {
+        }
+        for (uint32_t j = tid; j < Sc; j += blockDim.x) s_cnt[j] = 0;
+        __syncthreads();
+        // a3.2 in-chunk conflicts, one work unit per (survivor j, aligned group of 32 earlier
+        // survivors): a bit mask of the conflicting ones, appended to j's adjacency list
+        // (s_adj, up to kPAdj entries, any order; s_cnt[j] > kPAdj marks an overflow)
+        const uint32_t ng = (Sc + 31) / 32;
+        for (uint32_t u = tid; u < ng * Sc; u += blockDim.x) {
+            const uint32_t g = u / Sc, j = u - g * Sc;       // warps share g: broadcast reads
+            if (32 * g >= j) continue;
+            const uint32_t vj = s_val[j], kn = min(32u, j - 32 * g);
+            uint32_t mask = 0;
+            if (kn == 32) {
 #pragma unroll
-                        for (int t = 0; t < 32; ++t)
-                            mask |= (uint32_t)p_conflict(a, vj, s_val[k0 + t]) << t;
-                    } else {
-                        for (uint32_t t = 0; t < kn; ++t)
-                            mask |= (uint32_t)p_conflict(a, vj, s_val[k0 + t]) << t;
-                    }
-                    while (mask) {
-                        const uint32_t t = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        if (cnt < kPAdj) s_adj[j * kPAdj + cnt] = (uint16_t)(k0 + t);
-                        ++cnt;
-                    }
-                }
-                rchk += j + A;
-                s_adjn[j] = cnt > kPAdj ? 255 : (uint8_t)cnt;
-                if (a.timing && cnt > kPAdj) atomicAdd(&st->n_overflow, 1ull);
-                s_status[j] = prev ? 0 : (cnt ? 2 : 1);
-                confl += cnt;
+                for (int t = 0; t < 32; ++t) mask |= (uint32_t)p_conflict(a, vj, s_val[32 * g + t]) << t;
+            } else {
+                for (uint32_t t = 0; t < kn; ++t) mask |= (uint32_t)p_conflict(a, vj, s_val[32 * g + t]) << t;
             }
-            __syncthreads();
-            P_TR(1)
-            // Parallel rounds: an undecided survivor is rejected as soon as one earlier
-            // conflicting survivor is accepted, accepted once all of them are rejected.  Long
-            // dependency chains are finished by warp 0 walking the undecided ones in rank
-            // order.  A survivor is accepted iff no earlier ACCEPTED survivor conflicts.
-            int left = 0;
-            for (int round = 0; round < 8; ++round) {
-                int undecided = 0;
-                for (uint32_t j = tid; j < Sc; j += blockDim.x) {
-                    if (s_status[j] != 2) continue;
-                    const uint32_t na = s_adjn[j];
-                    bool acc_nb = false, und_nb = false;
-                    if (na != 255) {
-                        for (uint32_t t = 0; t < na; ++t) {
-                            const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
+            rchk += kn;
+            if (mask) {
+                uint32_t q = atomicAdd(&s_cnt[j], (uint32_t)__popc(mask));
+                while (mask) {
+                    const uint32_t t = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    if (q < kPAdj) s_adj[j * kPAdj + q] = (uint16_t)(32 * g + t);
+                    ++q;
+                }
+            }
+        }
+        __syncthreads();
+        // status: 1 = accepted, 0 = rejected, 2 = undecided.  A survivor conflicting with a word
+        // accepted in an earlier chunk of this tile is rejected outright (multi-chunk tiles only).
+        P_TR(1)
+        // Survivors with more than kPAdj earlier conflicts ("overflow") are listed in s_ovf (up to
+        // kPOvf; s_cnt = kPOvfMark) and decided by a whole warp per node in the rounds below.
+        if (tid == 0) s_novf = 0;
+        __syncthreads();
+        for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+            const uint32_t vj = s_val[j];
+            bool prev = false;
+            for (uint32_t t = 0; t < A && !prev; ++t) prev = p_conflict(a, vj, __ldcg(a.codebook + M0 + t));
+            rchk += A;
+            const uint32_t cnt = s_cnt[j];
+            s_status[j] = prev ? 0 : (cnt ? 2 : 1);
+            confl += cnt;
+            if (cnt > kPAdj) {
+                if (a.timing) atomicAdd(&st->n_overflow, 1ull);
+                if (!prev) {
+                    const uint32_t o = atomicAdd(&s_novf, 1u);
+                    if (o < kPOvf) { s_ovf[o] = (uint16_t)j; s_cnt[j] = kPOvfMark; }
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t novf = min(s_novf, kPOvf);
+        P_TR(5)
+        // a3.3 parallel rounds: an undecided survivor is rejected as soon as one earlier
+        // conflicting survivor is accepted, accepted once all of them are rejected.  Long
+        // dependency chains are finished by warp 0 walking the undecided ones in rank order.
+        // A survivor is accepted iff no earlier ACCEPTED survivor conflicts.
+        int left = 0;
+        for (int round = 0; round < 8; ++round) {
+            int undecided = 0;
+            for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                if (s_status[j] != 2) continue;
+                const uint32_t cn = s_cnt[j];
+                if (cn == kPOvfMark) { undecided = 1; continue; }     // a warp decides it below
+                bool acc_nb = false, und_nb = false;
+                if (cn <= kPAdj) {
+                    for (uint32_t t = 0; t < cn; ++t) {
+                        const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
+                        acc_nb |= sk == 1;
+                        und_nb |= sk == 2;
+                    }
+                } else {
+                    const uint32_t vj = s_val[j];
+                    for (uint32_t k = 0; k < j; ++k) {
+                        if (p_conflict(a, vj, s_val[k])) {
+                            const uint8_t sk = s_status[k];
                             acc_nb |= sk == 1;
                             und_nb |= sk == 2;
                         }
-                    } else {
-                        const uint32_t vj = s_val[j];
-                        for (uint32_t k = 0; k < j; ++k) {
-                            if (p_conflict(a, vj, s_val[k])) {
-                                const uint8_t sk = s_status[k];
-                                acc_nb |= sk == 1;
-                                und_nb |= sk == 2;
-                            }
-                        }
                     }
-                    // a status read in the same round may be stale (2): that only delays
+                }
+                // a status read in the same round may be stale (2): that only delays
+                if (acc_nb) s_status[j] = 0;
+                else if (!und_nb) s_status[j] = 1;
+                else undecided = 1;
+            }
+            // listed overflow nodes: lanes scan the earlier survivors
+            for (uint32_t o = tid >> 5; o < novf; o += blockDim.x >> 5) {
+                const uint32_t j = s_ovf[o];
+                if (s_status[j] != 2) continue;                       // warp-uniform
+                const uint32_t vj = s_val[j];
+                bool acc_nb = false, und_nb = false;
+                for (uint32_t k = lane; k < j; k += 32) {
+                    if (p_conflict(a, vj, s_val[k])) {
+                        const uint8_t sk = s_status[k];
+                        acc_nb |= sk == 1;
+                        und_nb |= sk == 2;
+                    }
+                }
+                acc_nb = __any_sync(0xffffffffu, acc_nb);
+                und_nb = __any_sync(0xffffffffu, und_nb);
+                if (lane == 0) {
                     if (acc_nb) s_status[j] = 0;
                     else if (!und_nb) s_status[j] = 1;
-                    else undecided = 1;
-                }
-                if (a.timing && tid == 0) atomicAdd(&st->n_rounds, 1ull);
-                left = __syncthreads_or(undecided);
-                if (!left) break;
-            }
-            if (left && tid < 32) {
-                for (uint32_t j = 0; j < Sc; ++j) {
-                    if (s_status[j] != 2) continue;                 // warp-uniform
-                    if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
-                    const uint32_t na = s_adjn[j];
-                    bool acc_nb = false;
-                    if (na != 255) {
-                        if (lane < na) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
-                    } else {
-                        const uint32_t vj = s_val[j];
-                        for (uint32_t k = lane; k < j; k += 32)
-                            acc_nb |= (s_status[k] == 1) && p_conflict(a, vj, s_val[k]);
-                    }
-                    acc_nb = __any_sync(0xffffffffu, acc_nb);
-                    if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
-                    __syncwarp();
                 }
             }
-            __syncthreads();
-            P_TR(2)
-            // ordered append of the chunk's accepted survivors
-            for (uint32_t j0 = 0; j0 < Sc; j0 += blockDim.x) {
-                const uint32_t j = j0 + tid;
-                const uint32_t acc = (j < Sc && s_status[j] == 1) ? 1u : 0u;
-                uint32_t tot;
-                const uint32_t pos = A + p_block_scan(acc, &tot, s_ws);
-                if (acc) {
-                    if (M0 + pos < a.capacity) a.codebook[M0 + pos] = s_val[j];
-                    else st->error = 1;
-                    if (a.wdef_valid) wdef += a.N - 1 - (t0 + s_idx[j]);
-                }
-                A += tot;
-            }
-            if (A > a.capacity - M0) A = (uint32_t)(a.capacity - M0);
-            __threadfence_block();
-            __syncthreads();
-            P_TR(3)
+            if (a.timing && tid == 0) atomicAdd(&st->n_rounds, 1ull);
+            left = __syncthreads_or(undecided);
+            if (!left) break;
         }
-        // block-bound summaries of the words appended at [M0, M0 + A): AND / OR per block of 32
-        // and per super-block of 1024 (appends only ever narrow the AND and widen the OR)
-        if (a.bound && A) {
-            // thread t holds position (M0 & ~31) + t: warp w covers aligned block (M0 >> 5) + w
-            const unsigned long long e = M0 + A, p0 = M0 & ~31ull;
+        if (left && tid < 32) {
+            for (uint32_t j = 0; j < Sc; ++j) {
+                if (s_status[j] != 2) continue;                 // warp-uniform
+                if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
+                const uint32_t cn = s_cnt[j];
+                bool acc_nb = false;
+                if (cn <= kPAdj) {
+                    if (lane < cn) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
+                } else {
+                    const uint32_t vj = s_val[j];
+                    for (uint32_t k = lane; k < j; k += 32)
+                        acc_nb |= (s_status[k] == 1) && p_conflict(a, vj, s_val[k]);
+                }
+                acc_nb = __any_sync(0xffffffffu, acc_nb);
+                if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        P_TR(2)
+        // a4 ordered append of the chunk's accepted survivors; their values are also staged in
+        // order (in s_adj, free now) for the block-bound summaries
+        uint32_t *s_stage = reinterpret_cast<uint32_t *>(s_adj);
+        const uint32_t A_start = A;
+        for (uint32_t j0 = 0; j0 < Sc; j0 += blockDim.x) {
+            const uint32_t j = j0 + tid;
+            const uint32_t acc = (j < Sc && s_status[j] == 1) ? 1u : 0u;
+            uint32_t tot;
+            const uint32_t pos = A + p_block_scan(acc, &tot, s_ws);
+            if (acc) {
+                const unsigned long long p = M0 + pos;
+                const uint32_t v = s_val[j];
+                s_stage[pos - A_start] = v;
+                if (p < a.capacity) {
+                    a.codebook[p] = v;
+                } else {
+                    st->error = 1;
+                }
+                if (a.wdef_valid) wdef += a.N - 1 - (t0 + s_idx[j]);
+            }
+            A += tot;
+        }
+        __syncthreads();
+        if (a.bound && A > A_start) {
+            // AND / OR per aligned block of 32 (warp w of the loop covers one block) and per
+            // super-block of 1024; appends only ever narrow the AND and widen the OR.  The
+            // reductions are fire-and-forget; the grid barrier after the commit publishes them.
+            const unsigned long long b = M0 + A_start, e = min(M0 + A, (unsigned long long)a.capacity);
+            const unsigned long long p0 = b & ~31ull;
             for (unsigned long long p = p0 + tid; p < ((e + 31) & ~31ull); p += blockDim.x) {
-                const bool in = p >= M0 && p < e;
-                const uint32_t w = in ? __ldcg(a.codebook + p) : 0u;
+                const bool in = p >= b && p < e;
+                const uint32_t w = in ? s_stage[p - b] : 0u;
                 const uint32_t an = __reduce_and_sync(0xffffffffu, in ? w : ~0u);
                 const uint32_t orr = __reduce_or_sync(0xffffffffu, w);
                 if (lane == 0) {
-                    const unsigned long long k = p >> 5;
-                    atomicAnd(a.bAnd + k, an);
-                    atomicOr(a.bOr + k, orr);
-                    atomicAnd(a.sAnd + (k >> 5), an);
-                    atomicOr(a.sOr + (k >> 5), orr);
+                    atomicAnd(&a.bsum[p >> 5].x, an);
+                    atomicOr(&a.bsum[p >> 5].y, orr);
+                    atomicAnd(&a.ssum[p >> 10].x, an);
+                    atomicOr(&a.ssum[p >> 10].y, orr);
                 }
             }
         }
-        // clear per-tile state for the next tile
-        for (uint32_t w = tid; w < words; w += blockDim.x) a.dead[w] = 0;
-        // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            rchk += __shfl_down_sync(0xffffffffu, rchk, o);
-            confl += __shfl_down_sync(0xffffffffu, confl, o);
-            wdef += __shfl_down_sync(0xffffffffu, wdef, o);
-        }
-        if (lane == 0) {
-            if (rchk) atomicAdd(&s_stat[0], rchk);
-            if (confl) atomicAdd(&s_stat[1], confl);
-            if (wdef) atomicAdd(&s_stat[2], wdef);
-        }
+        if (A > a.capacity - M0) A = (uint32_t)(a.capacity - M0);
+        __threadfence_block();
         __syncthreads();
-        if (tid == 0) {
-            st->resolve_checks += s_stat[0];
-            st->conflicts += s_stat[1];
-            st->w_def += s_stat[2];
-        }
-        P_TR(4)
-        if (tid == 0) {
-            unsigned long long M1 = M0 + A;
-            if (M1 > a.capacity) M1 = a.capacity;
-            st->M = M1;
-            if (a.weight_bound) {
-                // first index of each weight among the words just appended (acceptance
-                // order is weight-sorted for graded orders); stored +1, 0 = none yet
-                for (unsigned long long p = M0; p < M1; ++p) {
-                    const uint32_t w = __popc(a.codebook[p]);
-                    if (p == 0 || __popc(a.codebook[p - 1]) != w)
-                        if (!st->wfirst[w]) st->wfirst[w] = (unsigned int)(p + 1);
-                }
+        P_TR(3)
+    }
+    // clear per-tile state for the next tile
+    for (uint32_t w = tid; w < words; w += blockDim.x) a.dead[w] = 0;
+    if (tid < kPMaxLevels) st->item_ctr[tid] = 0;
+    // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        rchk += __shfl_down_sync(0xffffffffu, rchk, o);
+        confl += __shfl_down_sync(0xffffffffu, confl, o);
+        wdef += __shfl_down_sync(0xffffffffu, wdef, o);
+    }
+    if (lane == 0) {
+        if (rchk) atomicAdd(&s_stat[0], rchk);
+        if (confl) atomicAdd(&s_stat[1], confl);
+        if (wdef) atomicAdd(&s_stat[2], wdef);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        st->resolve_checks += s_stat[0];
+        st->conflicts += s_stat[1];
+        st->w_def += s_stat[2];
+    }
+    P_TR(4)
+    if (tid == 0) {
+        unsigned long long M1 = M0 + A;
+        if (M1 > a.capacity) M1 = a.capacity;
+        st->M = M1;
+        if (a.weight_bound) {
+            // first index of each weight among the words just appended (acceptance
+            // order is weight-sorted for graded orders); stored +1, 0 = none yet
+            for (unsigned long long p = M0; p < M1; ++p) {
+                const uint32_t w = __popc(a.codebook[p]);
+                if (p == 0 || __popc(a.codebook[p - 1]) != w)
+                    if (!st->wfirst[w]) st->wfirst[w] = (unsigned int)(p + 1);
             }
-            if (S) { st->S_last = S; st->K_last = K; }
-            st->K_next = p_next_tile(a, K, S, A, t0 + K, M1, st->S_last, st->K_last ? st->K_last : 1u);
-            st->survivors += S;
-            st->tiles += 1;
-            st->levels += L;
         }
-        __threadfence();
-    
+        if (S) { st->S_last = S; st->K_last = K; }
+        st->K_next = p_next_tile(a, K, S, A, t0 + K, M1, st->S_last, st->K_last ? st->K_last : 1u);
+        st->survivors += S;
+        st->tiles += 1;
+        st->levels += L;
+    }
+    __threadfence();
 }
 
 template <int kMinBlocks>
@@ -764,9 +970,9 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     uint32_t *s_val = reinterpret_cast<uint32_t *>(p_dyn);
     uint16_t *s_idx = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 4);
     uint8_t *s_status = p_dyn + kPChunk * 6;
-    uint8_t *s_adjn = p_dyn + kPChunk * 7;
-    uint16_t *s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 8);
-    uint32_t *s_pre = reinterpret_cast<uint32_t *>(p_dyn + p_resolve_smem(kPChunk));
+    uint32_t *s_cnt = reinterpret_cast<uint32_t *>(p_dyn + kPChunk * 8);
+    uint16_t *s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 12);
+    uint32_t *s_pre = reinterpret_cast<uint32_t *>(p_dyn + p_scratch_smem(kPChunk));
     uint32_t *s_live = s_pre + kPMaxTile / 32 + 4;
     __shared__ uint32_t s_basis[32];
     PState *st = a.st;
@@ -783,8 +989,9 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     unsigned long long my_checks = 0;
     PSmem sm;
     sm.C = C; sm.off = off; sm.s_basis = s_basis; sm.s_ws = s_ws; sm.s_val = s_val; sm.s_idx = s_idx;
-    sm.s_status = s_status; sm.s_adjn = s_adjn; sm.s_adj = s_adj; sm.chunk = kPChunk;
+    sm.s_status = s_status; sm.s_cnt = s_cnt; sm.s_adj = s_adj; sm.chunk = kPChunk;
 
+    PTimers tmr = {};
     unsigned long long t0 = a.part_mode ? a.t_single : a.t_begin;
     while (t0 < a.t_end) {
         const unsigned long long M = __ldcg(&st->M);
@@ -802,7 +1009,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
         const unsigned long long base = p_base(a, t0, M);
         const int L = p_levels(M - base, a.W0, a.growth);
         const uint32_t W0 = a.W0;
-        const bool timer = a.timing && blockIdx.x == 0 && threadIdx.x == 0;
+        PTimers *timer = (a.timing && blockIdx.x == 0 && threadIdx.x == 0) ? &tmr : nullptr;
         unsigned long long tm = timer ? p_now() : 0, tm_tile = tm;
 
         const uint32_t words = (K + 31) / 32;
@@ -857,9 +1064,22 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             PLevel lv;
             lv.l = l; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
             lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0;
-            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = pwords; lv.basis = s_basis; lv.c_lo = c_lo; lv.w_base = w_lo * 32;
+            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = pwords; lv.basis = s_basis; lv.stage = reinterpret_cast<uint32_t *>(p_dyn); lv.c_lo = c_lo; lv.w_base = w_lo * 32;
             const unsigned long long items = (unsigned long long)B * nsub;
-            for (unsigned long long it = gwarp; it < items; it += nwarps) {
+            if (timer) {
+                const unsigned long long t = p_now();
+                timer->prefix[l] += t - tm;
+                timer->live[l] += n_l;
+                timer->items_n[l] += items;
+            }
+            unsigned long long t_it = a.timing ? p_now() : 0;
+            // items: the first one per warp static, the rest claimed dynamically (one global
+            // atomic per item, issued before the current item so its latency hides behind it);
+            // partition mode keeps a static stride (its counters are not reset between launches)
+            unsigned int claim = 0;
+            unsigned long long it = gwarp;
+            if (!a.part_mode && it < items && lane == 0) claim = atomicAdd(&st->item_ctr[l], 1u);
+            while (it < items) {
                 if (a.so) {
                     if (R == 2) p_item<2, 1>(a, lv, it, C, off, my_checks);
                     else p_item<1, 1>(a, lv, it, C, off, my_checks);
@@ -873,28 +1093,58 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                 } else {
                     p_item<1, 0>(a, lv, it, C, off, my_checks);
                 }
+                if (a.timing && (threadIdx.x & 31) == 0) {
+                    const unsigned long long t = p_now();
+                    atomicAdd(&st->t_item_sum[l], t - t_it);
+                    atomicMax(&st->t_item_max[l & 1], t - t_it);
+                    t_it = t;
+                }
+                if (a.part_mode) {
+                    it += nwarps;
+                } else {
+                    it = nwarps + __shfl_sync(0xffffffffu, claim, 0);
+                    if (it < items && lane == 0) claim = atomicAdd(&st->item_ctr[l], 1u);
+                }
             }
             if (a.timing) {
                 unsigned long long dc = my_checks - checks_before;
                 for (int o = 16; o > 0; o >>= 1) dc += __shfl_down_sync(0xffffffffu, dc, o);
                 if ((threadIdx.x & 31) == 0 && dc) atomicAdd(&st->c_level[l], dc);
+                if ((threadIdx.x & 31) == 0) atomicMax(&st->t_item_end[l & 1], p_now());
             }
             grid.sync();
-            if (timer) { const unsigned long long t = p_now(); st->t_level[l] += t - tm; tm = t; }
+            if (timer) {
+                const unsigned long long t = p_now(), e = __ldcg(&st->t_item_end[l & 1]);
+                st->t_item_end[l & 1] = 0;
+                timer->item_max[l] += __ldcg(&st->t_item_max[l & 1]);
+                st->t_item_max[l & 1] = 0;
+                timer->level[l] += t - tm;
+                timer->items[l] += e > tm ? e - tm : 0;
+                tm = t;
+            }
         }
 
         if (a.part_mode) break;       // the host runs the exchange and k_resolve_tile
         // ------------------------------------------------ resolve + commit (CTA 0)
         if (blockIdx.x == 0) p_resolve(a, sm, t0, K, L, timer, tm);
-        if (timer) { const unsigned long long t = p_now(); st->t_resolve += t - tm; tm = t; }
+        if (timer) { const unsigned long long t = p_now(); timer->resolve += t - tm; tm = t; }
         grid.sync();
-        if (timer) { const unsigned long long t = p_now(); st->t_sync += t - tm; st->t_tile += t - tm_tile; }
+        if (timer) { const unsigned long long t = p_now(); timer->sync += t - tm; timer->tile += t - tm_tile; }
         t0 += K;
     }
     // work counter: lanes hold per-lane counts
     for (int o = 16; o > 0; o >>= 1) my_checks += __shfl_down_sync(0xffffffffu, my_checks, o);
     if (lane == 0 && my_checks) atomicAdd(&st->checks_exec, my_checks);
     if (!a.part_mode && blockIdx.x == 0 && threadIdx.x == 0) *a.d_count = st->M;
+    if (a.timing && blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int l = 0; l < kPMaxLevels; ++l) {
+            st->t_level[l] = tmr.level[l]; st->t_items[l] = tmr.items[l];
+            st->t_prefix[l] = tmr.prefix[l]; st->n_live[l] = tmr.live[l]; st->n_items[l] = tmr.items_n[l];
+            st->t_itmax[l] = tmr.item_max[l];
+        }
+        for (int i = 0; i < 6; ++i) st->t_r[i] = tmr.r[i];
+        st->t_resolve = tmr.resolve; st->t_sync = tmr.sync; st->t_tile = tmr.tile;
+    }
 }
 
 // partition mode, one tile: survivors -> resolve -> commit by one CTA (all ranks identically)
@@ -916,14 +1166,14 @@ __global__ void __launch_bounds__(kPThreads, 1) k_resolve_tile(PArgs a) {
     sm.s_val = reinterpret_cast<uint32_t *>(p_dyn);
     sm.s_idx = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 4);
     sm.s_status = p_dyn + kPChunk * 6;
-    sm.s_adjn = p_dyn + kPChunk * 7;
-    sm.s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 8);
+    sm.s_cnt = reinterpret_cast<uint32_t *>(p_dyn + kPChunk * 8);
+    sm.s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 12);
     sm.chunk = kPChunk;
     const unsigned long long M = __ldcg(&a.st->M);
     uint32_t K = a.K_single;
     if ((unsigned long long)K > a.t_end - a.t_single) K = (uint32_t)(a.t_end - a.t_single);
     const int L = p_levels(M - p_base(a, a.t_single, M), a.W0, a.growth);
-    p_resolve(a, sm, a.t_single, K, L, false, 0);
+    p_resolve(a, sm, a.t_single, K, L, nullptr, 0);
     if (threadIdx.x == 0) *a.d_count = a.st->M;
 }
 
@@ -934,7 +1184,7 @@ struct PContext {
     uint32_t *vals = nullptr, *dead = nullptr;
     uint2 *q0 = nullptr, *q1 = nullptr, *surv = nullptr;
     uint8_t *status = nullptr;
-    uint32_t *bsum = nullptr;       // block-bound summaries: bAnd | bOr | sAnd | sOr
+    uint32_t *bsum = nullptr;       // block-bound summaries: (AND, OR) per block, then per super-block
     size_t bsum_words = 0;          // allocated u32 words
     PState *st = nullptr;
     OrderTables *tabs = nullptr;
@@ -1020,8 +1270,10 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
         PCK(cudaStreamSynchronize(s));   // k0 lives on this stack frame
     }
     PCK(cudaMemsetAsync(cx->dead, 0, kPMaxTile / 8, s));
-    // block-bound summaries for the whole capacity (AND = all ones, OR = 0 before any append)
-    const size_t nblk = (size_t)((r.capacity + 31) / 32) + 1, nsup = (size_t)((r.capacity + 1023) / 1024) + 1;
+    // block-bound summaries for the whole capacity, (AND, OR) pairs: AND = all ones, OR = 0
+    // before any append.  Blocks padded to whole super-blocks (a super-block's 32 block
+    // summaries are staged as one 256-byte run).
+    const size_t nsup = (size_t)((r.capacity + 1023) / 1024) + 1, nblk = nsup * 32;
     const size_t need = 2 * (nblk + nsup);
     if (cx->bsum_words < need) {
         if (cx->bsum) PCK(cudaFree(cx->bsum));
@@ -1030,23 +1282,22 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
         PCK(cudaMalloc(&cx->bsum, need * 4));
         cx->bsum_words = need;
     }
-    PCK(cudaMemsetAsync(cx->bsum, 0xff, nblk * 4, s));
-    PCK(cudaMemsetAsync(cx->bsum + nblk, 0, nblk * 4, s));
-    PCK(cudaMemsetAsync(cx->bsum + 2 * nblk, 0xff, nsup * 4, s));
-    PCK(cudaMemsetAsync(cx->bsum + 2 * nblk + nsup, 0, nsup * 4, s));
+    PCK(cudaMemsetAsync(cx->bsum, 0, need * 4, s));
+    PCK(cudaMemset2DAsync(cx->bsum, 8, 0xff, 4, nblk + nsup, s));     // the AND word of every pair
     PArgs a;
-    a.bAnd = cx->bsum;
-    a.bOr = cx->bsum + nblk;
-    a.sAnd = cx->bsum + 2 * nblk;
-    a.sOr = cx->bsum + 2 * nblk + nsup;
+    a.bsum = reinterpret_cast<uint2 *>(cx->bsum);
+    a.ssum = reinterpret_cast<uint2 *>(cx->bsum) + nblk;
     a.nmask = r.n >= 32 ? 0xffffffffu : ((1u << r.n) - 1u);
     a.n = (int)r.n; a.ord = r.ordering; a.d = r.d;
     a.N = 1ull << r.n;
     a.tile_min = r.opt.tile_min; a.tile_max = r.opt.tile_max ? r.opt.tile_max : kPDefaultTile;
     if (a.tile_min > a.tile_max) a.tile_min = a.tile_max;
     a.W0 = r.opt.window0;
-    a.growth = (int)(r.opt.growth ? r.opt.growth
-                                  : (!r.self_orthogonal && !(r.opt.flags & GC_FLAG_NO_BLOCK_BOUND)) ? 4u : 2u);
+    // default window growth: without the block bound x4 per level; with it, two levels (newest
+    // W0, then everything) for lex / Gray / B-orderings, where the bound skips almost all of a
+    // deep window, and x16 for graded orders, where it skips less and compaction pays
+    const bool bnd = !r.self_orthogonal && !(r.opt.flags & GC_FLAG_NO_BLOCK_BOUND);
+    a.growth = (int)(r.opt.growth ? r.opt.growth : !bnd ? 2u : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4u : 12u);
     a.mix = (r.d >= 2 && r.d <= 4 && !(r.opt.flags & GC_FLAG_POPC_ONLY)) ? (int)r.d : 0;
     a.codebook = r.d_codebook; a.capacity = r.capacity;
     a.tabs = cx->tabs; a.vals = cx->vals; a.dead = cx->dead;
@@ -1056,7 +1307,10 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     a.bound = !r.self_orthogonal && !(r.opt.flags & GC_FLAG_NO_BLOCK_BOUND);
     // with the block bound most of a window is skipped by summary tests: one item per warp and
     // long sub-ranges keep a level to a few dependent round trips
-    a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP"))) : (a.bound ? 1 : 2);
+    // (graded orders, whose deep windows pass more blocks, balance better with more, smaller items:
+    // warps claim them dynamically)
+    a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP")))
+                       : !a.bound ? 2 : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4 : 1;
     a.sub_max_bound = getenv("GC_SUB_MAX") ? (uint32_t)std::max(64, atoi(getenv("GC_SUB_MAX"))) : 32768u;
     a.target_accepted = getenv("GC_TARGET_ACCEPTED") ? (uint32_t)std::max(1, atoi(getenv("GC_TARGET_ACCEPTED")))
                                                      : kPTargetAccepted;
@@ -1129,17 +1383,23 @@ static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a) {
             const double T = (double)full.tiles;
             fprintf(stderr, "[gc] persistent: %llu tiles, per tile: total %.2f us, resolve %.2f us, final sync %.2f us\n",
                     full.tiles, full.t_tile / T / 1e3, full.t_resolve / T / 1e3, full.t_sync / T / 1e3);
-            fprintf(stderr, "[gc]   resolve: gather %.2f conflicts %.2f sequential %.2f append %.2f clear+stats %.2f us\n",
-                    full.t_r[0] / T / 1e3, full.t_r[1] / T / 1e3, full.t_r[2] / T / 1e3, full.t_r[3] / T / 1e3,
-                    full.t_r[4] / T / 1e3);
+            fprintf(stderr, "[gc]   resolve: gather %.2f conflicts %.2f status %.2f rounds+sequential %.2f append %.2f "
+                    "clear+stats %.2f us\n", full.t_r[0] / T / 1e3, full.t_r[1] / T / 1e3, full.t_r[5] / T / 1e3,
+                    full.t_r[2] / T / 1e3, full.t_r[3] / T / 1e3, full.t_r[4] / T / 1e3);
             fprintf(stderr, "[gc]   resolve: per tile %.2f adjacency overflows, %.2f rounds, %.2f sequential nodes\n",
                     full.n_overflow / T, full.n_rounds / T, full.n_seq / T);
             for (int l = 0; l < kPMaxLevels; ++l)
                 if (full.t_level[l])
-                    fprintf(stderr, "[gc]   level %2d: %.3f s total (%.2f us per tile), %.3g checks, %.1f%% of the "
-                            "mixed/POPC peak (148 SM x 19.18/clk x 1965 MHz)\n", l, full.t_level[l] / 1e9,
-                            full.t_level[l] / T / 1e3, (double)full.c_level[l],
+                    fprintf(stderr, "[gc]   level %2d: %.3f s total (%.2f us per tile, last item done at %.2f us), %.3g "
+                            "checks, %.1f%% of the mixed/POPC peak (148 SM x 19.18/clk x 1965 MHz)\n", l, full.t_level[l] / 1e9,
+                            full.t_level[l] / T / 1e3, full.t_items[l] / T / 1e3, (double)full.c_level[l],
                             100.0 * (double)full.c_level[l] / (full.t_level[l] * 1e-9) / (148.0 * 19.18 * 1.965e9));
+            for (int l = 0; l < kPMaxLevels; ++l)
+                if (full.t_level[l])
+                    fprintf(stderr, "[gc]   level %2d: per tile %.1f live candidates, %.1f items; prefix %.2f us, "
+                            "warp item mean %.2f us, longest %.2f us\n", l, full.n_live[l] / T, full.n_items[l] / T,
+                            full.t_prefix[l] / T / 1e3, full.t_item_sum[l] / (double)std::max(1ull, full.n_items[l]) / 1e3,
+                            full.t_itmax[l] / T / 1e3);
         }
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }
