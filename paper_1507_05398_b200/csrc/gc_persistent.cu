@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "gc_internal.h"
 #include "gc_order.cuh"
@@ -655,6 +656,28 @@ __device__ __forceinline__ unsigned long long p_base(const PArgs &a, unsigned lo
     return M;
 }
 
+// Commit-side state and counters, kept by the CTA that resolves (thread 0) in its shared memory
+// so the tile's critical path has no global read-modify-write; loaded from / flushed to PState
+// once per kernel.  M and K_next are also published to PState every tile (fire-and-forget
+// stores the grid barrier makes visible).
+struct PCount {
+    unsigned long long M, survivors, tiles, levels, resolve_checks, conflicts, w_def;
+    unsigned int S_last, K_last;
+    unsigned int wfirst[33];
+};
+__device__ __forceinline__ void p_count_load(PCount &pc, const PState *st) {
+    pc.M = st->M; pc.survivors = st->survivors; pc.tiles = st->tiles; pc.levels = st->levels;
+    pc.resolve_checks = st->resolve_checks; pc.conflicts = st->conflicts; pc.w_def = st->w_def;
+    pc.S_last = st->S_last; pc.K_last = st->K_last;
+    for (int w = 0; w < 33; ++w) pc.wfirst[w] = st->wfirst[w];
+}
+__device__ __forceinline__ void p_count_store(const PCount &pc, PState *st) {
+    st->M = pc.M; st->survivors = pc.survivors; st->tiles = pc.tiles; st->levels = pc.levels;
+    st->resolve_checks = pc.resolve_checks; st->conflicts = pc.conflicts; st->w_def = pc.w_def;
+    st->S_last = pc.S_last; st->K_last = pc.K_last;
+    for (int w = 0; w < 33; ++w) st->wfirst[w] = pc.wfirst[w];
+}
+
 // diagnostics (GC_DEBUG_PHASES): accumulated by thread 0 of CTA 0 in local memory, written once
 struct PTimers {
     unsigned long long level[kPMaxLevels], items[kPMaxLevels];
@@ -675,7 +698,7 @@ struct PSmem {
 };
 
 __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsigned long long t0, uint32_t K, int L,
-                                          PTimers *timer, unsigned long long tm) {
+                                          PCount &pc, PTimers *timer, unsigned long long tm) {
     const uint32_t kPChunk = sm.chunk;
     const uint32_t (*C)[33] = sm.C;
     const uint64_t *off = sm.off;
@@ -723,9 +746,11 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
     __shared__ unsigned long long s_stat[3];
     __shared__ uint16_t s_ovf[kPOvf];
     __shared__ uint32_t s_novf;
+    __shared__ uint32_t s_wmin[33];          // graded orders: first tile position of each weight
     if (tid < 3) s_stat[tid] = 0;
+    if (tid < 33) s_wmin[tid] = 0xffffffffu;
     unsigned long long rchk = 0, confl = 0, wdef = 0;
-    const unsigned long long M0 = __ldcg(&st->M);
+    const unsigned long long M0 = pc.M;
     uint32_t A = 0;                   // accepted so far in this tile (codebook[M0, M0+A))
     for (uint32_t c0 = 0; c0 < S; c0 += kPChunk) {
         const uint32_t Sc = min(kPChunk, S - c0);
@@ -742,28 +767,38 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         // survivors): a bit mask of the conflicting ones, appended to j's adjacency list
         // (s_adj, up to kPAdj entries, any order; s_cnt[j] > kPAdj marks an overflow)
         const uint32_t ng = (Sc + 31) / 32;
-        for (uint32_t u = tid; u < ng * Sc; u += blockDim.x) {
-            const uint32_t g = u / Sc, j = u - g * Sc;       // warps share g: broadcast reads
-            if (32 * g >= j) continue;
-            const uint32_t vj = s_val[j], kn = min(32u, j - 32 * g);
-            uint32_t mask = 0;
-            if (kn == 32) {
+        auto units = [&](auto so_tag) {
+            constexpr bool SO = decltype(so_tag)::value;
+            auto cf = [&](uint32_t u, uint32_t w) {
+                return (uint32_t)__popc(u ^ w) < a.d || (SO && (__popc(u & w) & 1));
+            };
+            for (uint32_t u = tid; u < ng * Sc; u += blockDim.x) {
+                const uint32_t g = u / Sc, j = u - g * Sc;       // warps share g: broadcast reads
+                if (32 * g < j) {
+                    const uint32_t vj = s_val[j], kn = min(32u, j - 32 * g);
+                    const uint32_t *sg = s_val + 32 * g;
+                    uint32_t mask = 0;
+                    if (kn == 32) {
 #pragma unroll
-                for (int t = 0; t < 32; ++t) mask |= (uint32_t)p_conflict(a, vj, s_val[32 * g + t]) << t;
-            } else {
-                for (uint32_t t = 0; t < kn; ++t) mask |= (uint32_t)p_conflict(a, vj, s_val[32 * g + t]) << t;
-            }
-            rchk += kn;
-            if (mask) {
-                uint32_t q = atomicAdd(&s_cnt[j], (uint32_t)__popc(mask));
-                while (mask) {
-                    const uint32_t t = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    if (q < kPAdj) s_adj[j * kPAdj + q] = (uint16_t)(32 * g + t);
-                    ++q;
+                        for (int t = 0; t < 32; ++t) mask |= (uint32_t)cf(vj, sg[t]) << t;
+                    } else {
+                        for (uint32_t t = 0; t < kn; ++t) mask |= (uint32_t)cf(vj, sg[t]) << t;
+                    }
+                    rchk += kn;
+                    if (mask) {
+                        uint32_t q = atomicAdd(&s_cnt[j], (uint32_t)__popc(mask));
+                        while (mask) {
+                            const uint32_t t = __ffs(mask) - 1;
+                            mask &= mask - 1;
+                            if (q < kPAdj) s_adj[j * kPAdj + q] = (uint16_t)(32 * g + t);
+                            ++q;
+                        }
+                    }
                 }
             }
-        }
+        };
+        if (a.so) units(std::true_type{});
+        else units(std::false_type{});
         __syncthreads();
         // status: 1 = accepted, 0 = rejected, 2 = undecided.  A survivor conflicting with a word
         // accepted in an earlier chunk of this tile is rejected outright (multi-chunk tiles only).
@@ -881,6 +916,7 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
                 const unsigned long long p = M0 + pos;
                 const uint32_t v = s_val[j];
                 s_stage[pos - A_start] = v;
+                if (a.weight_bound) atomicMin(&s_wmin[__popc(v)], pos);
                 if (p < a.capacity) {
                     a.codebook[p] = v;
                 } else {
@@ -932,31 +968,30 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
     }
     __syncthreads();
     if (tid == 0) {
-        st->resolve_checks += s_stat[0];
-        st->conflicts += s_stat[1];
-        st->w_def += s_stat[2];
+        pc.resolve_checks += s_stat[0];
+        pc.conflicts += s_stat[1];
+        pc.w_def += s_stat[2];
     }
     P_TR(4)
     if (tid == 0) {
         unsigned long long M1 = M0 + A;
         if (M1 > a.capacity) M1 = a.capacity;
+        pc.M = M1;
         st->M = M1;
-        if (a.weight_bound) {
-            // first index of each weight among the words just appended (acceptance
-            // order is weight-sorted for graded orders); stored +1, 0 = none yet
-            for (unsigned long long p = M0; p < M1; ++p) {
-                const uint32_t w = __popc(a.codebook[p]);
-                if (p == 0 || __popc(a.codebook[p - 1]) != w)
-                    if (!st->wfirst[w]) st->wfirst[w] = (unsigned int)(p + 1);
-            }
-        }
-        if (S) { st->S_last = S; st->K_last = K; }
-        st->K_next = p_next_tile(a, K, S, A, t0 + K, M1, st->S_last, st->K_last ? st->K_last : 1u);
-        st->survivors += S;
-        st->tiles += 1;
-        st->levels += L;
+        if (S) { pc.S_last = S; pc.K_last = K; }
+        st->K_next = p_next_tile(a, K, S, A, t0 + K, M1, pc.S_last, pc.K_last ? pc.K_last : 1u);
+        pc.survivors += S;
+        pc.tiles += 1;
+        pc.levels += L;
     }
-    __threadfence();
+    if (a.weight_bound && tid < 33 && s_wmin[tid] != 0xffffffffu && !pc.wfirst[tid] &&
+        M0 + s_wmin[tid] < a.capacity) {
+        // first codebook index of each weight (acceptance order is weight-sorted for graded
+        // orders); stored +1, 0 = none yet
+        pc.wfirst[tid] = (unsigned int)(M0 + s_wmin[tid] + 1);
+        st->wfirst[tid] = pc.wfirst[tid];
+    }
+    __syncthreads();
 }
 
 template <int kMinBlocks>
@@ -991,7 +1026,11 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     sm.C = C; sm.off = off; sm.s_basis = s_basis; sm.s_ws = s_ws; sm.s_val = s_val; sm.s_idx = s_idx;
     sm.s_status = s_status; sm.s_cnt = s_cnt; sm.s_adj = s_adj; sm.chunk = kPChunk;
 
-    PTimers tmr = {};
+    __shared__ PCount pc;                     // CTA 0: commit-side state (see PCount)
+    if (blockIdx.x == 0 && threadIdx.x == 0) p_count_load(pc, st);
+    // diagnostics accumulate in CTA 0's shared memory (only its thread 0 touches them)
+    __shared__ PTimers tmr;
+    if (a.timing && blockIdx.x == 0 && threadIdx.x == 0) memset(&tmr, 0, sizeof tmr);
     unsigned long long t0 = a.part_mode ? a.t_single : a.t_begin;
     while (t0 < a.t_end) {
         const unsigned long long M = __ldcg(&st->M);
@@ -1126,7 +1165,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
 
         if (a.part_mode) break;       // the host runs the exchange and k_resolve_tile
         // ------------------------------------------------ resolve + commit (CTA 0)
-        if (blockIdx.x == 0) p_resolve(a, sm, t0, K, L, timer, tm);
+        if (blockIdx.x == 0) p_resolve(a, sm, t0, K, L, pc, timer, tm);
         if (timer) { const unsigned long long t = p_now(); timer->resolve += t - tm; tm = t; }
         grid.sync();
         if (timer) { const unsigned long long t = p_now(); timer->sync += t - tm; timer->tile += t - tm_tile; }
@@ -1135,7 +1174,10 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     // work counter: lanes hold per-lane counts
     for (int o = 16; o > 0; o >>= 1) my_checks += __shfl_down_sync(0xffffffffu, my_checks, o);
     if (lane == 0 && my_checks) atomicAdd(&st->checks_exec, my_checks);
-    if (!a.part_mode && blockIdx.x == 0 && threadIdx.x == 0) *a.d_count = st->M;
+    if (!a.part_mode && blockIdx.x == 0 && threadIdx.x == 0) {
+        p_count_store(pc, st);
+        *a.d_count = pc.M;
+    }
     if (a.timing && blockIdx.x == 0 && threadIdx.x == 0) {
         for (int l = 0; l < kPMaxLevels; ++l) {
             st->t_level[l] = tmr.level[l]; st->t_items[l] = tmr.items[l];
@@ -1169,12 +1211,18 @@ __global__ void __launch_bounds__(kPThreads, 1) k_resolve_tile(PArgs a) {
     sm.s_cnt = reinterpret_cast<uint32_t *>(p_dyn + kPChunk * 8);
     sm.s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 12);
     sm.chunk = kPChunk;
-    const unsigned long long M = __ldcg(&a.st->M);
+    __shared__ PCount pc;
+    if (threadIdx.x == 0) p_count_load(pc, a.st);
+    __syncthreads();
+    const unsigned long long M = pc.M;
     uint32_t K = a.K_single;
     if ((unsigned long long)K > a.t_end - a.t_single) K = (uint32_t)(a.t_end - a.t_single);
     const int L = p_levels(M - p_base(a, a.t_single, M), a.W0, a.growth);
-    p_resolve(a, sm, a.t_single, K, L, nullptr, 0);
-    if (threadIdx.x == 0) *a.d_count = a.st->M;
+    p_resolve(a, sm, a.t_single, K, L, pc, nullptr, 0);
+    if (threadIdx.x == 0) {
+        p_count_store(pc, a.st);
+        *a.d_count = pc.M;
+    }
 }
 
 // ------------------------------------------------------------------ host side
