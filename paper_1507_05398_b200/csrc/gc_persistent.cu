@@ -36,7 +36,7 @@ namespace gc {
 
 constexpr int kPThreads = 512;              // threads per CTA (16 warps); grid = #SMs
 constexpr int kPWarps = kPThreads / 32;
-constexpr uint32_t kPR2Min = 0;             // levels with >= this many candidates use 2 per lane
+constexpr uint32_t kPR2Min = 1;             // levels with >= this many candidates use 2 per lane
 constexpr uint32_t kPSubMin = 64;           // codewords per warp item: at least ...
 constexpr uint32_t kPSubMax = 2048;         // ... and at most
 constexpr int kPMaxLevels = 32;
@@ -48,15 +48,17 @@ constexpr uint32_t kPMaxPredictedSurvivors = 1024;
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 constexpr uint32_t kPStageWords = 32 * 32;      // per-warp stage: 32 blocks of 32 codewords (4 KiB)
 constexpr uint32_t kPWarpStage = kPStageWords + 8 * 64 + 32;   // + 8 super-blocks' block summaries + a block queue
+constexpr uint32_t kPWinWords = 4096 + 32;      // level-0 window copied to shared memory (words, then
+                                                // kPWinWords / 32 + 1 block summaries)
 constexpr uint32_t kPOvf = 1024;                // overflow survivors decided warp-parallel (per chunk)
 constexpr uint32_t kPOvfMark = 0xffffffffu;     // s_cnt of a listed overflow survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + pad (1 B) + s_cnt (4 B) + s_adj (2 B x kPAdj)
 __host__ __device__ constexpr size_t p_resolve_smem(uint32_t chunk) { return (size_t)chunk * (12 + 2 * kPAdj); }
 // + level prefix: s_pre[kPMaxTile/32 + 1] and s_live[kPMaxTile/32]
 // the level stages (kPWarpStage words per warp) alias the resolve scratch: a CTA never runs both
+constexpr size_t kPLevelSmem = (size_t)kPWarps * kPWarpStage * 4 + kPWinWords * 4 + (kPWinWords / 32 + 1) * 8;
 __host__ __device__ constexpr size_t p_scratch_smem(uint32_t chunk) {
-    return p_resolve_smem(chunk) > (size_t)kPWarps * kPWarpStage * 4 ? p_resolve_smem(chunk)
-                                                                      : (size_t)kPWarps * kPWarpStage * 4;
+    return p_resolve_smem(chunk) > kPLevelSmem ? p_resolve_smem(chunk) : kPLevelSmem;
 }
 __host__ __device__ constexpr size_t p_dyn_smem(uint32_t chunk) {
     return p_scratch_smem(chunk) + (size_t)(2 * (kPMaxTile / 32) + 4) * 4;
@@ -74,7 +76,7 @@ struct PState {
     unsigned long long t_level[kPMaxLevels];   // diagnostics: CTA 0's view, ns (%globaltimer)
     unsigned long long c_level[kPMaxLevels];   // diagnostics: lane-checks per level
     unsigned long long t_resolve, t_sync, t_tile;
-    unsigned long long t_r[6];                 // resolve sub-steps
+    unsigned long long t_r[8];                 // resolve sub-steps
     unsigned long long t_items[kPMaxLevels];   // diagnostics: level start -> last item done (any warp)
     unsigned long long t_item_end[2];          // per-level scratch (alternating slots)
     unsigned long long t_item_max[2];          // per-level scratch: longest warp item
@@ -416,6 +418,36 @@ __device__ __forceinline__ bool p_scan_list(const PArgs &a, long long lo, long l
     return false;
 }
 
+// scan [lo, hi) newest first with the block bound, the window and its block summaries held in
+// shared memory (level 0): lane t tests block kt - t, the warp checks the passing blocks
+// straight from shared memory -- no global round trip at all
+template <int R, int MIX>
+__device__ __forceinline__ uint32_t p_scan_window(const PArgs &a, const uint32_t *win, const uint2 *wsum,
+                                                  long long win_lo, long long lo, long long hi, uint32_t cA,
+                                                  uint32_t cO, const uint32_t (&v)[R], uint32_t (&m)[R]) {
+    const int lane = threadIdx.x & 31;
+    uint32_t scanned = 0;
+    const long long kb = lo >> 5, k0 = win_lo >> 5;
+    for (long long kt = (hi - 1) >> 5; kt >= kb; kt -= 32) {
+        const long long k = kt - lane;
+        bool pass = false;
+        if (k >= kb) {
+            const uint2 bs = wsum[k - k0];
+            pass = p_lb(bs.x, bs.y, cA, cO, a.nmask) < a.d;
+        }
+        uint32_t mask = __ballot_sync(0xffffffffu, pass);
+        while (mask) {
+            const long long q = kt - (__ffs(mask) - 1);
+            mask &= mask - 1;
+            const int o_lo = (int)(max(lo, q << 5) - (q << 5)), o_hi = (int)(min(hi, (q + 1) << 5) - (q << 5));
+            p_block_smem<R, MIX>(win + ((q << 5) - win_lo), o_lo, o_hi, v, m);
+            scanned += (uint32_t)(o_hi - o_lo);
+            if (p_all_dead<R, MIX>(m, a.d)) return scanned;
+        }
+    }
+    return scanned;
+}
+
 // scan [lo, hi) newest first with the block bound.  Ranges up to 4096 codewords test their
 // blocks directly (p_scan_blocks).  Longer ones go down a hierarchy, newest first, with a
 // fixed number of dependent round trips per round whatever passes:
@@ -537,6 +569,9 @@ struct PLevel {
     uint32_t words;
     const uint32_t *basis;   // B-ordering basis (smem)
     uint32_t *stage;         // block-bound staging, kPStageWords per warp (smem; aliases the resolve scratch)
+    const uint32_t *win;     // level 0 with the block bound: the whole window, copied to shared memory
+    const uint2 *wsum;       //   once per CTA (words [win_lo, hi), win_lo = lo & ~31) and its block summaries
+    long long win_lo;
     uint32_t c_lo;           // first tile index of the screened range
     uint32_t w_base;         // 32 * (first mask word of the range)
 };
@@ -616,7 +651,8 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                 for (int r = 0; r < R; ++r)
                     if (live[r]) { la &= v[r]; lo_ |= v[r]; }
                 const uint32_t cA = __reduce_and_sync(0xffffffffu, la), cO = __reduce_or_sync(0xffffffffu, lo_);
-                sc = p_scan_bound<R, MIX>(a, s_lo, s_hi, cA, cO, v, m, lv.stage + (threadIdx.x >> 5) * kPWarpStage);
+                sc = lv.win ? p_scan_window<R, MIX>(a, lv.win, lv.wsum, lv.win_lo, s_lo, s_hi, cA, cO, v, m)
+                            : p_scan_bound<R, MIX>(a, s_lo, s_hi, cA, cO, v, m, lv.stage + (threadIdx.x >> 5) * kPWarpStage);
             } else {
                 sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
             }
@@ -682,7 +718,7 @@ __device__ __forceinline__ void p_count_store(const PCount &pc, PState *st) {
 struct PTimers {
     unsigned long long level[kPMaxLevels], items[kPMaxLevels];
     unsigned long long prefix[kPMaxLevels], live[kPMaxLevels], items_n[kPMaxLevels], item_max[kPMaxLevels];
-    unsigned long long resolve, sync, tile, r[6];
+    unsigned long long resolve, sync, tile, r[8];
 };
 
 struct PSmem {
@@ -711,6 +747,7 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
     const int lane = threadIdx.x & 31;
     const uint32_t words = (K + 31) / 32;
     const uint32_t tid = threadIdx.x;
+    const unsigned long long tg = timer ? clock64() : 0;
     if (L == 0) {      // empty codebook: no level ran, so the filters are applied here
         for (uint32_t i = tid; i < K; i += blockDim.x)
             if (!p_allowed(a, p_gen(a, C, off, s_basis, t0 + i))) atomicOr(&a.dead[i >> 5], 1u << (i & 31));
@@ -740,9 +777,10 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         S += tot;
     }
     __syncthreads();
-    unsigned long long tr = timer ? p_now() : 0;
-#define P_TR(i) if (timer) { const unsigned long long t_ = p_now(); timer->r[i] += t_ - tr; tr = t_; }
-    if (timer) timer->r[0] += tr - tm;
+    // resolve sub-steps timed with the SM cycle counter (one CTA: consistent, and cheap to read)
+    unsigned long long tr = timer ? clock64() : 0;
+#define P_TR(i) if (timer) { const unsigned long long t_ = clock64(); timer->r[i] += t_ - tr; tr = t_; }
+    if (timer) timer->r[0] += tr - tg;
     __shared__ unsigned long long s_stat[3];
     __shared__ uint16_t s_ovf[kPOvf];
     __shared__ uint32_t s_novf;
@@ -883,6 +921,7 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
             left = __syncthreads_or(undecided);
             if (!left) break;
         }
+        P_TR(6)
         if (left && tid < 32) {
             for (uint32_t j = 0; j < Sc; ++j) {
                 if (s_status[j] != 2) continue;                 // warp-uniform
@@ -1104,6 +1143,29 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             lv.l = l; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
             lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0;
             lv.s_pre = s_pre; lv.s_live = s_live; lv.words = pwords; lv.basis = s_basis; lv.stage = reinterpret_cast<uint32_t *>(p_dyn); lv.c_lo = c_lo; lv.w_base = w_lo * 32;
+            lv.win = nullptr; lv.wsum = nullptr; lv.win_lo = 0;
+            if (l == 0 && a.bound && !a.so && hi > lo && hi - (lo & ~31ll) <= (long long)kPWinWords) {
+                // level 0 with the block bound: every item scans part of the same small window,
+                // so each CTA copies it (and its block summaries) to shared memory once
+                uint32_t *win = reinterpret_cast<uint32_t *>(p_dyn + (size_t)kPWarps * kPWarpStage * 4);
+                uint2 *wsum = reinterpret_cast<uint2 *>(win + kPWinWords);
+                const long long wl = lo & ~31ll, nwd = hi - wl;
+                for (long long c = threadIdx.x; c < (nwd + 3) / 4; c += blockDim.x) {
+                    const unsigned long long w0 = (unsigned long long)(wl + 4 * c);
+                    if (w0 + 4 <= a.capacity) {
+                        p_cp_async16(win + 4 * c, a.codebook + w0);
+                    } else {
+                        for (int e = 0; e < 4; ++e)
+                            if (w0 + e < a.capacity) win[4 * c + e] = __ldcg(a.codebook + w0 + e);
+                    }
+                }
+                const long long nbk = ((hi - 1) >> 5) - (wl >> 5) + 1;
+                for (long long k = threadIdx.x; k < nbk; k += blockDim.x) wsum[k] = __ldcg(a.bsum + (wl >> 5) + k);
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                __syncthreads();
+                lv.win = win; lv.wsum = wsum; lv.win_lo = wl;
+            }
             const unsigned long long items = (unsigned long long)B * nsub;
             if (timer) {
                 const unsigned long long t = p_now();
@@ -1184,7 +1246,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             st->t_prefix[l] = tmr.prefix[l]; st->n_live[l] = tmr.live[l]; st->n_items[l] = tmr.items_n[l];
             st->t_itmax[l] = tmr.item_max[l];
         }
-        for (int i = 0; i < 6; ++i) st->t_r[i] = tmr.r[i];
+        for (int i = 0; i < 8; ++i) st->t_r[i] = tmr.r[i];
         st->t_resolve = tmr.resolve; st->t_sync = tmr.sync; st->t_tile = tmr.tile;
     }
 }
@@ -1431,9 +1493,10 @@ static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a) {
             const double T = (double)full.tiles;
             fprintf(stderr, "[gc] persistent: %llu tiles, per tile: total %.2f us, resolve %.2f us, final sync %.2f us\n",
                     full.tiles, full.t_tile / T / 1e3, full.t_resolve / T / 1e3, full.t_sync / T / 1e3);
-            fprintf(stderr, "[gc]   resolve: gather %.2f conflicts %.2f status %.2f rounds+sequential %.2f append %.2f "
-                    "clear+stats %.2f us\n", full.t_r[0] / T / 1e3, full.t_r[1] / T / 1e3, full.t_r[5] / T / 1e3,
-                    full.t_r[2] / T / 1e3, full.t_r[3] / T / 1e3, full.t_r[4] / T / 1e3);
+            fprintf(stderr, "[gc]   resolve: gather %.2f conflicts %.2f status %.2f rounds %.2f sequential %.2f append %.2f "
+                    "clear+stats %.2f us (SM cycles at 1965 MHz)\n", full.t_r[0] / T / 1965.0, full.t_r[1] / T / 1965.0,
+                    full.t_r[5] / T / 1965.0, full.t_r[6] / T / 1965.0, full.t_r[2] / T / 1965.0, full.t_r[3] / T / 1965.0,
+                    full.t_r[4] / T / 1965.0);
             fprintf(stderr, "[gc]   resolve: per tile %.2f adjacency overflows, %.2f rounds, %.2f sequential nodes\n",
                     full.n_overflow / T, full.n_rounds / T, full.n_seq / T);
             for (int l = 0; l < kPMaxLevels; ++l)
