@@ -23,7 +23,7 @@ $(SRC)/gc_analysis.o: $(SRC)/gc_analysis.cu $(SRC)/gc_internal.h include/gc.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_analysis.ptxas.log || (cat $(SRC)/gc_analysis.ptxas.log; false)
 
 $(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o $(SRC)/gc_persistent.o $(SRC)/gc_analysis.o
-	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl
+	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl -lpthread
 
 $(ORACLE): oracle/greedy_oracle.c
 	gcc -O2 -mpopcnt -Wall -shared -fPIC -o $@ $<

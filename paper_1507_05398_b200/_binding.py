@@ -189,7 +189,7 @@ def gc_capacity_bound(n: int, d: int) -> int:
 def gc_generate(n: int, d: int, ordering="lex", capacity: int | None = None) -> np.ndarray:
     """The greedy code (uint64 array, acceptance order) -- gc_generate()."""
     cap = gc_capacity_bound(n, d) if capacity is None else capacity
-    out = np.zeros(max(cap, 1), dtype=np.uint64)
+    out = np.empty(max(cap, 1), dtype=np.uint64)
     cnt = ctypes.c_uint64(cap)
     _check(_lib.gc_generate(n, d, ordering_id(ordering), out.ctypes.data_as(_u64p), ctypes.byref(cnt)),
            "gc_generate")
@@ -199,7 +199,7 @@ def gc_generate(n: int, d: int, ordering="lex", capacity: int | None = None) -> 
 def gc_generate_ex(n: int, d: int, ordering="lex", options=None, capacity: int | None = None):
     """(codewords uint64 array, stats dict) -- gc_generate_ex()."""
     cap = gc_capacity_bound(n, d) if capacity is None else capacity
-    out = np.zeros(max(cap, 1), dtype=np.uint64)
+    out = np.empty(max(cap, 1), dtype=np.uint64)
     cnt = ctypes.c_uint64(cap)
     st = gc_stats()
     st.struct_size = ctypes.sizeof(gc_stats)
@@ -246,7 +246,7 @@ def gc_construct(n: int, d: int, ordering="lex", basis=None, constant_weight=-1,
     gc_construct().  Returns (codewords uint64 array, stats dict)."""
     prob, keep = _problem(n, d, ordering, basis, constant_weight, self_orthogonal)
     cap = gc_capacity_bound(n, d) if capacity is None else capacity
-    out = np.zeros(max(cap, 1), dtype=np.uint64)
+    out = np.empty(max(cap, 1), dtype=np.uint64)
     cnt = ctypes.c_uint64(cap)
     st = gc_stats()
     st.struct_size = ctypes.sizeof(gc_stats)

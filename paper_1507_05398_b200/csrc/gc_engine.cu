@@ -37,6 +37,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gc_internal.h"
@@ -750,42 +751,94 @@ extern "C" int gc_generate_ex(uint32_t n, uint32_t d, gc_ordering ordering, cons
     return host_construct(a, out_codewords, out_count, stats);
 }
 
+// Host-buffer path: device codebook, count and a pinned staging buffer are cached per device
+// (grown on demand) so a call pays no allocation; the code comes back through pinned memory
+// and is widened to u64 by a few host threads.
+namespace {
+struct HostPathCache {
+    uint32_t *d_cb = nullptr;
+    uint64_t cap = 0;
+    unsigned long long *d_cnt = nullptr;
+    uint32_t *h_pin = nullptr;
+    uint64_t pin_cap = 0;
+    std::mutex mu;
+};
+std::mutex g_hp_mu;
+std::map<int, std::unique_ptr<HostPathCache>> g_hp;
+
+HostPathCache *host_cache(int dev) {
+    std::lock_guard<std::mutex> g(g_hp_mu);
+    auto &p = g_hp[dev];
+    if (!p) p.reset(new HostPathCache);
+    return p.get();
+}
+
+void widen(const uint32_t *src, uint64_t *dst, uint64_t M) {
+    const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+    const uint64_t per = (M + hw - 1) / hw;
+    if (M < (1u << 16) || hw == 1) {
+        for (uint64_t i = 0; i < M; ++i) dst[i] = src[i];
+        return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < hw; ++t) {
+        const uint64_t b = t * per, e = std::min(M, b + per);
+        if (b >= e) break;
+        th.emplace_back([=] { for (uint64_t i = b; i < e; ++i) dst[i] = src[i]; });
+    }
+    for (auto &x : th) x.join();
+}
+}  // namespace
+
 static int host_construct(RunArgs &a, uint64_t *out_codewords, uint64_t *out_count, gc_stats *stats) {
     int rc;
     const uint32_t n = a.n, d = a.d;
     const uint64_t cap = gc_capacity_bound(n, d);
-    uint32_t *d_cb = nullptr;
-    unsigned long long *d_cnt = nullptr;
-    CK(cudaMalloc(&d_cb, cap * sizeof(uint32_t)));
-    if (cudaMalloc(&d_cnt, sizeof(unsigned long long)) != cudaSuccess) {
-        cudaFree(d_cb);
-        set_error("cudaMalloc failed");
-        return GC_ENOMEM;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    HostPathCache *hc = host_cache(dev);
+    std::lock_guard<std::mutex> lock(hc->mu);
+    if (hc->cap < cap) {
+        if (hc->d_cb) cudaFree(hc->d_cb);
+        hc->d_cb = nullptr;
+        hc->cap = 0;
+        CK(cudaMalloc(&hc->d_cb, cap * sizeof(uint32_t)));
+        hc->cap = cap;
     }
+    if (!hc->d_cnt) CK(cudaMalloc(&hc->d_cnt, sizeof(unsigned long long)));
     gc_stats local{};
-    a.d_codebook = d_cb; a.capacity = cap; a.d_count = (uint64_t *)d_cnt;
+    a.d_codebook = hc->d_cb; a.capacity = cap; a.d_count = (uint64_t *)hc->d_cnt;
     a.stream = nullptr; a.stats = stats ? stats : &local;
     rc = engine_run(a);
     unsigned long long M = 0;
     if (rc == GC_OK) {
-        cudaError_t e = cudaMemcpy(&M, d_cnt, sizeof M, cudaMemcpyDeviceToHost);
+        cudaError_t e = cudaMemcpy(&M, hc->d_cnt, sizeof M, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); rc = GC_ECUDA; }
     }
     if (rc == GC_OK) {
         if (M > *out_count) {
             *out_count = M;
             rc = GC_ENOSPC;
-        } else {
-            std::vector<uint32_t> h(M);
-            cudaError_t e = cudaMemcpy(h.data(), d_cb, M * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+        } else if (M) {
+            if (hc->pin_cap < M) {
+                if (hc->h_pin) cudaFreeHost(hc->h_pin);
+                hc->h_pin = nullptr;
+                hc->pin_cap = 0;
+                if (cudaHostAlloc(&hc->h_pin, cap * sizeof(uint32_t), cudaHostAllocDefault) == cudaSuccess)
+                    hc->pin_cap = cap;
+            }
+            std::vector<uint32_t> pageable;
+            uint32_t *h = hc->h_pin;
+            if (!h) { pageable.resize(M); h = pageable.data(); }      // pinned allocation failed
+            cudaError_t e = cudaMemcpy(h, hc->d_cb, M * sizeof(uint32_t), cudaMemcpyDeviceToHost);
             if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); rc = GC_ECUDA; }
             else {
-                for (unsigned long long i = 0; i < M; ++i) out_codewords[i] = h[i];
+                widen(h, out_codewords, M);
                 *out_count = M;
             }
+        } else {
+            *out_count = 0;
         }
     }
-    cudaFree(d_cb);
-    cudaFree(d_cnt);
     return rc;
 }
