@@ -48,8 +48,10 @@ constexpr uint32_t kPMaxPredictedSurvivors = 1024;
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 constexpr uint32_t kPStageWords = 32 * 32;      // per-warp stage: 32 blocks of 32 codewords (4 KiB)
 constexpr uint32_t kPWarpStage = kPStageWords + 8 * 64 + 32;   // + 8 super-blocks' block summaries + a block queue
-constexpr uint32_t kPWinWords = 4096 + 32;      // level-0 window copied to shared memory (words, then
+constexpr uint32_t kPWinWords = 16384 + 32;     // level-0 window copied to shared memory (words, then
                                                 // kPWinWords / 32 + 1 block summaries)
+constexpr int kPSplitBits = 12;                 // a warp's live candidates differing in more bits are
+                                                // screened as two halves (block bound, p_item)
 constexpr uint32_t kPOvf = 1024;                // overflow survivors decided warp-parallel (per chunk)
 constexpr uint32_t kPOvfMark = 0xffffffffu;     // s_cnt of a listed overflow survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + pad (1 B) + s_cnt (4 B) + s_adj (2 B x kPAdj)
@@ -651,8 +653,40 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                 for (int r = 0; r < R; ++r)
                     if (live[r]) { la &= v[r]; lo_ |= v[r]; }
                 const uint32_t cA = __reduce_and_sync(0xffffffffu, la), cO = __reduce_or_sync(0xffffffffu, lo_);
-                sc = lv.win ? p_scan_window<R, MIX>(a, lv.win, lv.wsum, lv.win_lo, s_lo, s_hi, cA, cO, v, m)
-                            : p_scan_bound<R, MIX>(a, s_lo, s_hi, cA, cO, v, m, lv.stage + (threadIdx.x >> 5) * kPWarpStage);
+                uint32_t *stg = lv.stage + (threadIdx.x >> 5) * kPWarpStage;
+                auto scan = [&](uint32_t sA, uint32_t sO, uint32_t (&mm)[R]) {
+                    return lv.win ? p_scan_window<R, MIX>(a, lv.win, lv.wsum, lv.win_lo, s_lo, s_hi, sA, sO, v, mm)
+                                  : p_scan_bound<R, MIX>(a, s_lo, s_hi, sA, sO, v, mm, stg);
+                };
+                const uint32_t vary = cO & ~cA;            // bits on which the live candidates differ
+                // (not for graded orders: a weight class in colex order varies many bits by
+                // nature, and the weight bound already cuts their windows)
+                if (__popc(vary) <= kPSplitBits || (a.ord >= GRADED_LEX && !a.use_basis)) {
+                    sc = scan(cA, cO, m);
+                } else {
+                    // weak consensus (typically a batch straddling a carry of a high bit): scan
+                    // the two halves split on the highest varying bit separately, each with its
+                    // own, much stronger, consensus; the other half's lanes ride along as dead
+                    const uint32_t hb = 1u << (31 - __clz(vary));
+                    sc = 0;
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        uint32_t ha = ~0u, ho = 0u, mm[R];
+                        bool any_h = false;
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            const bool in = live[r] && (((v[r] & hb) != 0) == (half == 1));
+                            mm[r] = in ? m[r] : 0u;
+                            if (in) { ha &= v[r]; ho |= v[r]; any_h = true; }
+                        }
+                        if (!__any_sync(0xffffffffu, any_h)) continue;
+                        const uint32_t hA = __reduce_and_sync(0xffffffffu, ha), hO = __reduce_or_sync(0xffffffffu, ho);
+                        sc += scan(hA, hO, mm);
+#pragma unroll
+                        for (int r = 0; r < R; ++r)
+                            if (live[r] && (((v[r] & hb) != 0) == (half == 1))) m[r] = mm[r];
+                    }
+                }
             } else {
                 sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
             }
