@@ -87,7 +87,6 @@ struct PState {
     unsigned long long n_overflow, n_seq, n_rounds;
     unsigned int error;
     unsigned int K_next;                       // size of the next tile (set by CTA 0)
-    unsigned int item_ctr[kPMaxLevels];        // dynamic item claims per level (reset by the resolve)
     unsigned int S_last, K_last;               // last tile with survivors: its S and K
     unsigned int wfirst[33];                   // graded orders: 1 + index of the first codeword of weight w
 };
@@ -1026,7 +1025,6 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
     }
     // clear per-tile state for the next tile
     for (uint32_t w = tid; w < words; w += blockDim.x) a.dead[w] = 0;
-    if (tid < kPMaxLevels) st->item_ctr[tid] = 0;
     // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1083,6 +1081,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     uint32_t *s_pre = reinterpret_cast<uint32_t *>(p_dyn + p_scratch_smem(kPChunk));
     uint32_t *s_live = s_pre + kPMaxTile / 32 + 4;
     __shared__ uint32_t s_basis[32];
+    __shared__ unsigned int s_claim;            // per-level item claims of this CTA
     PState *st = a.st;
     if (threadIdx.x < 32) s_basis[threadIdx.x] = a.basis[threadIdx.x];
     const bool graded = a.ord >= GRADED_LEX;
@@ -1092,7 +1091,6 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const uint32_t gwarp = blockIdx.x * kPWarps + (threadIdx.x >> 5);
     const uint32_t nwarps = gridDim.x * kPWarps;
     unsigned long long my_checks = 0;
     PSmem sm;
@@ -1208,13 +1206,17 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                 timer->items_n[l] += items;
             }
             unsigned long long t_it = a.timing ? p_now() : 0;
-            // items: the first one per warp static, the rest claimed dynamically (one global
-            // atomic per item, issued before the current item so its latency hides behind it);
-            // partition mode keeps a static stride (its counters are not reset between launches)
-            unsigned int claim = 0;
-            unsigned long long it = gwarp;
-            if (!a.part_mode && it < items && lane == 0) claim = atomicAdd(&st->item_ctr[l], 1u);
-            while (it < items) {
+            // items: CTA c owns items c, c + G, c + 2G, ...; its warps claim them in order from a
+            // shared-memory counter (dynamic balance inside the CTA, no global atomics -- one
+            // global counter for ~2400 warps serialises at L2 for microseconds)
+            if (threadIdx.x == 0) s_claim = 0;
+            __syncthreads();
+            while (true) {
+                unsigned int q = 0;
+                if (lane == 0) q = atomicAdd(&s_claim, 1u);
+                q = __shfl_sync(0xffffffffu, q, 0);
+                const unsigned long long it = blockIdx.x + (unsigned long long)q * gridDim.x;
+                if (it >= items) break;
                 if (a.so) {
                     if (R == 2) p_item<2, 1>(a, lv, it, C, off, my_checks);
                     else p_item<1, 1>(a, lv, it, C, off, my_checks);
@@ -1233,12 +1235,6 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                     atomicAdd(&st->t_item_sum[l], t - t_it);
                     atomicMax(&st->t_item_max[l & 1], t - t_it);
                     t_it = t;
-                }
-                if (a.part_mode) {
-                    it += nwarps;
-                } else {
-                    it = nwarps + __shfl_sync(0xffffffffu, claim, 0);
-                    if (it < items && lane == 0) claim = atomicAdd(&st->item_ctr[l], 1u);
                 }
             }
             if (a.timing) {
