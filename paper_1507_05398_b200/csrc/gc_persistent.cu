@@ -87,6 +87,7 @@ struct PState {
     unsigned long long n_overflow, n_seq, n_rounds;
     unsigned int error;
     unsigned int K_next;                       // size of the next tile (set by CTA 0)
+    unsigned long long token;                  // commit token: (tile + 1) << 39 | log2(K_next) << 34 | M
     unsigned int S_last, K_last;               // last tile with survivors: its S and K
     unsigned int wfirst[33];                   // graded orders: 1 + index of the first codeword of weight w
 };
@@ -731,7 +732,7 @@ __device__ __forceinline__ unsigned long long p_base(const PArgs &a, unsigned lo
 // stores the grid barrier makes visible).
 struct PCount {
     unsigned long long M, survivors, tiles, levels, resolve_checks, conflicts, w_def;
-    unsigned int S_last, K_last;
+    unsigned int S_last, K_last, K_next;
     unsigned int wfirst[33];
 };
 __device__ __forceinline__ void p_count_load(PCount &pc, const PState *st) {
@@ -1050,7 +1051,8 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         pc.M = M1;
         st->M = M1;
         if (S) { pc.S_last = S; pc.K_last = K; }
-        st->K_next = p_next_tile(a, K, S, A, t0 + K, M1, pc.S_last, pc.K_last ? pc.K_last : 1u);
+        pc.K_next = p_next_tile(a, K, S, A, t0 + K, M1, pc.S_last, pc.K_last ? pc.K_last : 1u);
+        st->K_next = pc.K_next;
         pc.survivors += S;
         pc.tiles += 1;
         pc.levels += L;
@@ -1102,10 +1104,16 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     // diagnostics accumulate in CTA 0's shared memory (only its thread 0 touches them)
     __shared__ PTimers tmr;
     if (a.timing && blockIdx.x == 0 && threadIdx.x == 0) memset(&tmr, 0, sizeof tmr);
+    // tile state every thread carries: the codebook size and the next tile size, as published
+    // by the commit token (no barrier and no load of M / K_next after a resolve)
+    unsigned long long curM = __ldcg(&st->M);
+    uint32_t curK = __ldcg(&st->K_next);
+    unsigned long long tile_no = 0;
+    __shared__ unsigned long long s_tok;
     unsigned long long t0 = a.part_mode ? a.t_single : a.t_begin;
     while (t0 < a.t_end) {
-        const unsigned long long M = __ldcg(&st->M);
-        uint32_t K = a.part_mode ? a.K_single : __ldcg(&st->K_next);
+        const unsigned long long M = curM;
+        uint32_t K = a.part_mode ? a.K_single : curK;
         if ((unsigned long long)K > a.t_end - t0) K = (uint32_t)(a.t_end - t0);
         // candidate range screened by this launch: the tile, or one rank's partition of it
         const uint32_t c_lo = a.part_mode ? min(a.part_lo, K) : 0u;
@@ -1257,10 +1265,35 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
 
         if (a.part_mode) break;       // the host runs the exchange and k_resolve_tile
         // ------------------------------------------------ resolve + commit (CTA 0)
-        if (blockIdx.x == 0) p_resolve(a, sm, t0, K, L, pc, timer, tm);
-        if (timer) { const unsigned long long t = p_now(); timer->resolve += t - tm; tm = t; }
-        grid.sync();
-        if (timer) { const unsigned long long t = p_now(); timer->sync += t - tm; timer->tile += t - tm_tile; }
+        // Commit token instead of a grid barrier: every other CTA finished this tile's levels
+        // (the last level's barrier), so the commit only has to be broadcast.  CTA 0 resolves,
+        // then publishes (release) the token carrying M and log2(K_next); the others wait for it
+        // (acquire) and take M and K from it -- no second barrier, no load of M / K_next.
+        ++tile_no;
+        const unsigned long long gen = tile_no & ((1ull << 25) - 1);
+        if (blockIdx.x == 0) {
+            p_resolve(a, sm, t0, K, L, pc, timer, tm);        // ends with __syncthreads
+            if (threadIdx.x == 0) {
+                const unsigned long long tok = (gen << 39) | ((unsigned long long)(31 - __clz(pc.K_next)) << 34) | pc.M;
+                __threadfence();
+                asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&st->token), "l"(tok) : "memory");
+            }
+            curM = pc.M;
+            curK = pc.K_next;
+            if (timer) { const unsigned long long t = p_now(); timer->resolve += t - tm; tm = t; }
+        } else {
+            if (threadIdx.x == 0) {
+                unsigned long long tok;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(tok) : "l"(&st->token) : "memory");
+                } while ((tok >> 39) != gen);
+                s_tok = tok;
+            }
+            __syncthreads();
+            curM = s_tok & ((1ull << 34) - 1);
+            curK = 1u << ((s_tok >> 34) & 31);
+        }
+        if (timer) { const unsigned long long t = p_now(); timer->tile += t - tm_tile; }
         t0 += K;
     }
     // work counter: lanes hold per-lane counts
