@@ -844,27 +844,31 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
             auto cf = [&](uint32_t u, uint32_t w) {
                 return (uint32_t)__popc(u ^ w) < a.d || (SO && (__popc(u & w) & 1));
             };
-            for (uint32_t u = tid; u < ng * Sc; u += blockDim.x) {
-                const uint32_t g = u / Sc, j = u - g * Sc;       // warps share g: broadcast reads
-                if (32 * g < j) {
-                    const uint32_t vj = s_val[j], kn = min(32u, j - 32 * g);
-                    const uint32_t *sg = s_val + 32 * g;
-                    uint32_t mask = 0;
-                    if (kn == 32) {
+            // warp task p = block pair (jb, kg <= jb): lane t holds survivor 32 jb + t, the 32
+            // survivors of group kg are broadcast by shuffles (no division, no idle lanes but on
+            // the diagonal)
+            const uint32_t ntask = ng * (ng + 1) / 2;
+            for (uint32_t p = tid >> 5; p < ntask; p += blockDim.x >> 5) {
+                uint32_t jb = (uint32_t)((sqrtf(8.0f * (float)p + 1.0f) - 1.0f) * 0.5f);
+                while ((jb + 1) * (jb + 2) / 2 <= p) ++jb;
+                while (jb * (jb + 1) / 2 > p) --jb;
+                const uint32_t kg = p - jb * (jb + 1) / 2;
+                const uint32_t j = 32 * jb + lane, k = 32 * kg + lane;
+                const uint32_t vj = j < Sc ? s_val[j] : 0u, vk = k < Sc ? s_val[k] : 0u;
+                uint32_t mask = 0;
 #pragma unroll
-                        for (int t = 0; t < 32; ++t) mask |= (uint32_t)cf(vj, sg[t]) << t;
-                    } else {
-                        for (uint32_t t = 0; t < kn; ++t) mask |= (uint32_t)cf(vj, sg[t]) << t;
-                    }
-                    rchk += kn;
-                    if (mask) {
-                        uint32_t q = atomicAdd(&s_cnt[j], (uint32_t)__popc(mask));
-                        while (mask) {
-                            const uint32_t t = __ffs(mask) - 1;
-                            mask &= mask - 1;
-                            if (q < kPAdj) s_adj[j * kPAdj + q] = (uint16_t)(32 * g + t);
-                            ++q;
-                        }
+                for (int t = 0; t < 32; ++t) mask |= (uint32_t)cf(vj, __shfl_sync(0xffffffffu, vk, t)) << t;
+                const uint32_t kmax = min(j, Sc);                 // earlier survivors only
+                const uint32_t lim = kmax > 32 * kg ? min(32u, kmax - 32 * kg) : 0u;
+                mask &= lim >= 32 ? 0xffffffffu : ((1u << lim) - 1u);
+                if (j < Sc) rchk += lim;
+                if (j < Sc && mask) {
+                    uint32_t q = atomicAdd(&s_cnt[j], (uint32_t)__popc(mask));
+                    while (mask) {
+                        const uint32_t t = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        if (q < kPAdj) s_adj[j * kPAdj + q] = (uint16_t)(32 * kg + t);
+                        ++q;
                     }
                 }
             }
