@@ -43,7 +43,8 @@ constexpr int kPMaxLevels = 32;
 constexpr uint32_t kPMaxTile = 1u << 16;    // largest tile (tile indices fit in 16 bits)
 // survivors resolved per chunk (shared memory): 4096 with one CTA per SM, 2048 with two
 constexpr uint32_t kPMaxBatches = kPMaxTile / 32;
-constexpr uint32_t kPTargetAccepted = 256;  // adaptive tiles grow up to ~2x this many accepted words
+constexpr uint32_t kPTargetAccepted = 384;  // adaptive tiles grow up to ~2x this many accepted words
+                                            // (graded orders: twice that)
 constexpr uint32_t kPMaxPredictedSurvivors = 1024;
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 constexpr uint32_t kPStageWords = 32 * 32;      // per-warp stage: 32 blocks of 32 codewords (4 KiB)
@@ -52,7 +53,8 @@ constexpr uint32_t kPWinWords = 16384 + 32;     // level-0 window copied to shar
                                                 // kPWinWords / 32 + 1 block summaries)
 constexpr int kPSplitBits = 12;                 // a warp's live candidates differing in more bits are
                                                 // screened as two halves (block bound, p_item)
-constexpr uint32_t kPOvf = 1024;                // overflow survivors decided warp-parallel (per chunk)
+constexpr uint32_t kPOvf = 1024;
+constexpr uint32_t kPResolveTmp = 2048;         // k_resolve_tile: staging words after the scratch                // overflow survivors decided warp-parallel (per chunk)
 constexpr uint32_t kPOvfMark = 0xffffffffu;     // s_cnt of a listed overflow survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + pad (1 B) + s_cnt (4 B) + s_adj (2 B x kPAdj)
 __host__ __device__ constexpr size_t p_resolve_smem(uint32_t chunk) { return (size_t)chunk * (12 + 2 * kPAdj); }
@@ -85,9 +87,11 @@ struct PState {
     unsigned long long t_item_sum[kPMaxLevels];
     unsigned long long t_prefix[kPMaxLevels], n_live[kPMaxLevels], n_items[kPMaxLevels], t_itmax[kPMaxLevels];
     unsigned long long n_overflow, n_seq, n_rounds;
+    unsigned long long n_chunked, s_max, n_rounds_max;   // diagnostics: multi-chunk tiles, largest S
     unsigned int error;
     unsigned int K_next;                       // size of the next tile (set by CTA 0)
-    unsigned long long token;                  // commit token: (tile + 1) << 39 | log2(K_next) << 34 | M
+    unsigned long long token;                  // commit token: (tile + 1) << 40 | partial << 39 | log2(K_next) << 34 | M
+    unsigned int K_used;                       // a partial tile's length (token bit 39)
     unsigned int S_last, K_last;               // last tile with survivors: its S and K
     unsigned int wfirst[33];                   // graded orders: 1 + index of the first codeword of weight w
 };
@@ -104,6 +108,7 @@ struct PArgs {
     int items_per_warp;             // target work items per warp and level
     uint32_t target_accepted;       // adaptive tiles grow toward ~this many accepted words per tile
     uint32_t sub_max_bound;         // longest window sub-range per warp item with the block bound
+    uint32_t partial_s;             // persistent engine: a tile with more survivors is cut after this many
     // partition mode (multi-GPU / emulated ranks): one tile's screen over one candidate range
     int part_mode;
     unsigned long long t_single;
@@ -732,7 +737,7 @@ __device__ __forceinline__ unsigned long long p_base(const PArgs &a, unsigned lo
 // stores the grid barrier makes visible).
 struct PCount {
     unsigned long long M, survivors, tiles, levels, resolve_checks, conflicts, w_def;
-    unsigned int S_last, K_last, K_next;
+    unsigned int S_last, K_last, K_next, K_used;
     unsigned int wfirst[33];
 };
 __device__ __forceinline__ void p_count_load(PCount &pc, const PState *st) {
@@ -765,10 +770,12 @@ struct PSmem {
     uint32_t *s_cnt;
     uint16_t *s_adj;
     uint32_t chunk;
+    uint32_t *s_tmp;          // staging for words accepted in earlier chunks of a tile
+    uint32_t tmp_words;
 };
 
 __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsigned long long t0, uint32_t K, int L,
-                                          PCount &pc, PTimers *timer, unsigned long long tm) {
+                                          PCount &pc, PTimers *timer, unsigned long long tm, bool allow_partial) {
     const uint32_t kPChunk = sm.chunk;
     const uint32_t (*C)[33] = sm.C;
     const uint64_t *off = sm.off;
@@ -811,10 +818,26 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         S += tot;
     }
     __syncthreads();
+    // Partial tile (persistent engine): with more survivors than one chunk, only the candidates
+    // ranked before the first survivor of the second chunk are decided now; the tile is cut
+    // there (K_used) and the rest is screened again as part of the next tile, against a codebook
+    // that then holds this chunk's accepted words.  Exact (tile boundaries never change the
+    // result) and it bounds a resolve to one chunk -- dense early tiles otherwise cost
+    // milliseconds in the multi-chunk path.
+    uint32_t K_used = K;
+    const uint32_t s_cut = min(kPChunk, a.partial_s);
+    if (allow_partial && S > s_cut) {
+        K_used = s_cut < kPChunk ? s_idx[s_cut] : __ldcg(&a.surv[kPChunk].x);
+        S = s_cut;
+    }
     // resolve sub-steps timed with the SM cycle counter (one CTA: consistent, and cheap to read)
     unsigned long long tr = timer ? clock64() : 0;
 #define P_TR(i) if (timer) { const unsigned long long t_ = clock64(); timer->r[i] += t_ - tr; tr = t_; }
     if (timer) timer->r[0] += tr - tg;
+    if (a.timing && tid == 0) {
+        atomicMax(&st->s_max, (unsigned long long)S);
+        if (S > kPChunk) atomicAdd(&st->n_chunked, 1ull);
+    }
     __shared__ unsigned long long s_stat[3];
     __shared__ uint16_t s_ovf[kPOvf];
     __shared__ uint32_t s_novf;
@@ -883,11 +906,31 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         // kPOvf; s_cnt = kPOvfMark) and decided by a whole warp per node in the rounds below.
         if (tid == 0) s_novf = 0;
         __syncthreads();
+        if (A > 0) {
+            // multi-chunk tiles: a survivor conflicting with a word accepted in an earlier chunk is
+            // rejected.  Those A words are staged through shared memory newest first (coalesced
+            // loads, one round trip per block) and every survivor is checked from there; s_status
+            // holds the verdict (1 = conflict) until the status pass below.
+            for (uint32_t j = tid; j < Sc; j += blockDim.x) s_status[j] = 0;
+            for (uint32_t top = A; top > 0;) {
+                const uint32_t nb = min(sm.tmp_words, top), b0 = top - nb;
+                __syncthreads();
+                for (uint32_t t = tid; t < nb; t += blockDim.x) sm.s_tmp[t] = __ldcg(a.codebook + M0 + b0 + t);
+                __syncthreads();
+                for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                    if (s_status[j]) continue;
+                    const uint32_t vj = s_val[j];
+                    bool c = false;
+                    for (uint32_t t = nb; t > 0 && !c; --t) c = p_conflict(a, vj, sm.s_tmp[t - 1]);
+                    rchk += nb;
+                    if (c) s_status[j] = 1;
+                }
+                top = b0;
+            }
+            __syncthreads();
+        }
         for (uint32_t j = tid; j < Sc; j += blockDim.x) {
-            const uint32_t vj = s_val[j];
-            bool prev = false;
-            for (uint32_t t = 0; t < A && !prev; ++t) prev = p_conflict(a, vj, __ldcg(a.codebook + M0 + t));
-            rchk += A;
+            const bool prev = A > 0 && s_status[j] != 0;
             const uint32_t cnt = s_cnt[j];
             s_status[j] = prev ? 0 : (cnt ? 2 : 1);
             confl += cnt;
@@ -955,7 +998,10 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
                     else if (!und_nb) s_status[j] = 1;
                 }
             }
-            if (a.timing && tid == 0) atomicAdd(&st->n_rounds, 1ull);
+            if (a.timing && tid == 0) {
+                atomicAdd(&st->n_rounds, 1ull);
+                atomicMax(&st->n_rounds_max, (unsigned long long)round + 1);
+            }
             left = __syncthreads_or(undecided);
             if (!left) break;
         }
@@ -1054,8 +1100,11 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         if (M1 > a.capacity) M1 = a.capacity;
         pc.M = M1;
         st->M = M1;
-        if (S) { pc.S_last = S; pc.K_last = K; }
-        pc.K_next = p_next_tile(a, K, S, A, t0 + K, M1, pc.S_last, pc.K_last ? pc.K_last : 1u);
+        if (S) { pc.S_last = S; pc.K_last = K_used; }
+        // (tile sizes stay powers of two: a partial tile's length is rounded down first)
+        pc.K_next = p_next_tile(a, 1u << (31 - __clz(K_used)), S, A, t0 + K_used, M1, pc.S_last,
+                                pc.K_last ? pc.K_last : 1u);
+        pc.K_used = K_used;
         st->K_next = pc.K_next;
         pc.survivors += S;
         pc.tiles += 1;
@@ -1102,6 +1151,8 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     PSmem sm;
     sm.C = C; sm.off = off; sm.s_basis = s_basis; sm.s_ws = s_ws; sm.s_val = s_val; sm.s_idx = s_idx;
     sm.s_status = s_status; sm.s_cnt = s_cnt; sm.s_adj = s_adj; sm.chunk = kPChunk;
+    sm.s_tmp = s_pre;                            // the level prefix is not used during a resolve
+    sm.tmp_words = 2 * (kPMaxTile / 32);
 
     __shared__ PCount pc;                     // CTA 0: commit-side state (see PCount)
     if (blockIdx.x == 0 && threadIdx.x == 0) p_count_load(pc, st);
@@ -1114,6 +1165,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     uint32_t curK = __ldcg(&st->K_next);
     unsigned long long tile_no = 0;
     __shared__ unsigned long long s_tok;
+    __shared__ uint32_t s_kused;
     unsigned long long t0 = a.part_mode ? a.t_single : a.t_begin;
     while (t0 < a.t_end) {
         const unsigned long long M = curM;
@@ -1274,31 +1326,38 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
         // then publishes (release) the token carrying M and log2(K_next); the others wait for it
         // (acquire) and take M and K from it -- no second barrier, no load of M / K_next.
         ++tile_no;
-        const unsigned long long gen = tile_no & ((1ull << 25) - 1);
+        const unsigned long long gen = tile_no & ((1ull << 24) - 1);
+        uint32_t K_used = K;
         if (blockIdx.x == 0) {
-            p_resolve(a, sm, t0, K, L, pc, timer, tm);        // ends with __syncthreads
+            p_resolve(a, sm, t0, K, L, pc, timer, tm, true);  // ends with __syncthreads
+            const bool partial = pc.K_used != K;
             if (threadIdx.x == 0) {
-                const unsigned long long tok = (gen << 39) | ((unsigned long long)(31 - __clz(pc.K_next)) << 34) | pc.M;
+                if (partial) st->K_used = pc.K_used;
+                const unsigned long long tok = (gen << 40) | ((unsigned long long)partial << 39) |
+                                               ((unsigned long long)(31 - __clz(pc.K_next)) << 34) | pc.M;
                 __threadfence();
                 asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&st->token), "l"(tok) : "memory");
             }
             curM = pc.M;
             curK = pc.K_next;
+            K_used = pc.K_used;
             if (timer) { const unsigned long long t = p_now(); timer->resolve += t - tm; tm = t; }
         } else {
             if (threadIdx.x == 0) {
                 unsigned long long tok;
                 do {
                     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(tok) : "l"(&st->token) : "memory");
-                } while ((tok >> 39) != gen);
+                } while ((tok >> 40) != gen);
                 s_tok = tok;
+                s_kused = ((tok >> 39) & 1) ? __ldcg(&st->K_used) : K;
             }
             __syncthreads();
             curM = s_tok & ((1ull << 34) - 1);
             curK = 1u << ((s_tok >> 34) & 31);
+            K_used = s_kused;
         }
         if (timer) { const unsigned long long t = p_now(); timer->tile += t - tm_tile; }
-        t0 += K;
+        t0 += K_used;
     }
     // work counter: lanes hold per-lane counts
     for (int o = 16; o > 0; o >>= 1) my_checks += __shfl_down_sync(0xffffffffu, my_checks, o);
@@ -1340,6 +1399,8 @@ __global__ void __launch_bounds__(kPThreads, 1) k_resolve_tile(PArgs a) {
     sm.s_cnt = reinterpret_cast<uint32_t *>(p_dyn + kPChunk * 8);
     sm.s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 12);
     sm.chunk = kPChunk;
+    sm.s_tmp = reinterpret_cast<uint32_t *>(p_dyn + p_resolve_smem(kPChunk));
+    sm.tmp_words = kPResolveTmp;
     __shared__ PCount pc;
     if (threadIdx.x == 0) p_count_load(pc, a.st);
     __syncthreads();
@@ -1347,7 +1408,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_resolve_tile(PArgs a) {
     uint32_t K = a.K_single;
     if ((unsigned long long)K > a.t_end - a.t_single) K = (uint32_t)(a.t_end - a.t_single);
     const int L = p_levels(M - p_base(a, a.t_single, M), a.W0, a.growth);
-    p_resolve(a, sm, a.t_single, K, L, pc, nullptr, 0);
+    p_resolve(a, sm, a.t_single, K, L, pc, nullptr, 0, false);
     if (threadIdx.x == 0) {
         p_count_store(pc, a.st);
         *a.d_count = pc.M;
@@ -1489,8 +1550,10 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP")))
                        : !a.bound ? 2 : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4 : 1;
     a.sub_max_bound = getenv("GC_SUB_MAX") ? (uint32_t)std::max(64, atoi(getenv("GC_SUB_MAX"))) : 32768u;
+    a.partial_s = getenv("GC_PARTIAL_S") ? (uint32_t)std::max(32, atoi(getenv("GC_PARTIAL_S")))
+                  : (r.ordering >= GRADED_LEX && !r.use_basis) ? 1024u : 512u;
     a.target_accepted = getenv("GC_TARGET_ACCEPTED") ? (uint32_t)std::max(1, atoi(getenv("GC_TARGET_ACCEPTED")))
-                                                     : kPTargetAccepted;
+                        : (r.ordering >= GRADED_LEX && !r.use_basis) ? 2 * kPTargetAccepted : kPTargetAccepted;
     a.use_basis = r.use_basis;
     for (int i = 0; i < 32; ++i) a.basis[i] = r.basis[i];
     a.so = r.self_orthogonal;
@@ -1564,8 +1627,9 @@ static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a) {
                     "clear+stats %.2f us (SM cycles at 1965 MHz)\n", full.t_r[0] / T / 1965.0, full.t_r[1] / T / 1965.0,
                     full.t_r[5] / T / 1965.0, full.t_r[6] / T / 1965.0, full.t_r[2] / T / 1965.0, full.t_r[3] / T / 1965.0,
                     full.t_r[4] / T / 1965.0);
-            fprintf(stderr, "[gc]   resolve: per tile %.2f adjacency overflows, %.2f rounds, %.2f sequential nodes\n",
-                    full.n_overflow / T, full.n_rounds / T, full.n_seq / T);
+            fprintf(stderr, "[gc]   resolve: per tile %.2f adjacency overflows, %.2f rounds, %.2f sequential nodes; "
+                    "largest S %llu, %llu multi-chunk tiles, most rounds %llu\n",
+                    full.n_overflow / T, full.n_rounds / T, full.n_seq / T, full.s_max, full.n_chunked, full.n_rounds_max);
             for (int l = 0; l < kPMaxLevels; ++l)
                 if (full.t_level[l])
                     fprintf(stderr, "[gc]   level %2d: %.3f s total (%.2f us per tile, last item done at %.2f us), %.3g "
@@ -1609,7 +1673,7 @@ int persistent_run_partitioned(const RunArgs &r) {
     const size_t smem = p_dyn_smem(a.chunk);
     PCK(cudaFuncSetAttribute((const void *)k_construct<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     PCK(cudaFuncSetAttribute((const void *)k_resolve_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)p_resolve_smem(a.chunk)));
+                             (int)(p_resolve_smem(a.chunk) + kPResolveTmp * 4)));
     int per_sm = 0;
     PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_construct<1>, kPThreads, smem));
     if (per_sm < 1) { set_error("k_construct cannot be resident"); return GC_ECUDA; }
@@ -1639,7 +1703,7 @@ int persistent_run_partitioned(const RunArgs &r) {
             rc = nccl_allgather_u32(cx->dead + (size_t)r.rank * seg, cx->dead, seg, r.nccl_comm, s);
             if (rc) return rc;
         }
-        k_resolve_tile<<<1, kPThreads, p_resolve_smem(a.chunk), s>>>(a);
+        k_resolve_tile<<<1, kPThreads, p_resolve_smem(a.chunk) + kPResolveTmp * 4, s>>>(a);
         ++launches;
         PCK(cudaGetLastError());
         t0 += K;
