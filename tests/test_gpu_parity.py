@@ -244,3 +244,23 @@ def test_rank_entry_world1(gc):
     M = int(cnt.item())
     assert st["M"] == M
     assert np.array_equal(cb[:M].cpu().numpy().view(np.uint32), O.greedy_ball(n, d, o))
+
+
+# ------------------------------------------------ engine knobs (environment, read per call)
+
+ENV_KNOBS = [
+    {"GC_PARTIAL_S": "32"},                     # cut almost every tile after 32 survivors
+    {"GC_PARTIAL_S": "4096", "GC_TARGET_ACCEPTED": "2048"},   # big tiles, multi-chunk resolves
+    {"GC_GRID": "1"},                           # one CTA does every level and every resolve
+    {"GC_GRID": "3", "GC_ITEMS_PER_WARP": "8"},
+    {"GC_SUB_MAX": "64"},                       # many tiny deep-level items
+]
+
+
+@pytest.mark.parametrize("env", ENV_KNOBS, ids=lambda e: "-".join(f"{k}{v}" for k, v in e.items()))
+@pytest.mark.parametrize("n,d,o", [(18, 3, "lex"), (17, 4, "gray"), (16, 3, "glex"), (15, 5, "grlex")])
+def test_engine_knobs_invariance(gc, env, n, d, o, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w, st = gpu_code(gc, n, d, o)
+    assert np.array_equal(w, O.greedy_ball(n, d, o)), env
