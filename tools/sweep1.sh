@@ -1,1 +1,2 @@
-timeout 300 python tools/sweep.py '[{"cfg":[24,3,"lex"],"opts":{"emulate_ranks":2}},{"cfg":[26,4,"gray"],"opts":{"emulate_ranks":2}},{"cfg":[24,8,"lex"],"opts":{"emulate_ranks":2}},{"cfg":[28,3,"lex"],"opts":{"emulate_ranks":2}}]'
+C='[{"cfg":[28,3,"lex"]},{"cfg":[26,4,"gray"]},{"cfg":[24,3,"lex"]}]'
+for S in 65536 262144 524288 1048576; do echo "== submax $S"; GC_SUB_MAX=$S timeout 100 python tools/sweep.py "$C"; done
