@@ -838,11 +838,10 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         atomicMax(&st->s_max, (unsigned long long)S);
         if (S > kPChunk) atomicAdd(&st->n_chunked, 1ull);
     }
-    __shared__ unsigned long long s_stat[3];
+    __shared__ unsigned long long s_stat[kPWarps][3];
     __shared__ uint16_t s_ovf[kPOvf];
     __shared__ uint32_t s_novf;
     __shared__ uint32_t s_wmin[33];          // graded orders: first tile position of each weight
-    if (tid < 3) s_stat[tid] = 0;
     if (tid < 33) s_wmin[tid] = 0xffffffffu;
     unsigned long long rchk = 0, confl = 0, wdef = 0;
     const unsigned long long M0 = pc.M;
@@ -1076,23 +1075,23 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
     }
     // clear per-tile state for the next tile
     for (uint32_t w = tid; w < words; w += blockDim.x) a.dead[w] = 0;
-    // per-warp reduction first (64-bit shared atomics are emulated with CAS loops)
+    // per-warp reduction, then thread 0 sums the warps' partials (no 64-bit shared atomics,
+    // which are emulated with CAS loops)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         rchk += __shfl_down_sync(0xffffffffu, rchk, o);
         confl += __shfl_down_sync(0xffffffffu, confl, o);
         wdef += __shfl_down_sync(0xffffffffu, wdef, o);
     }
-    if (lane == 0) {
-        if (rchk) atomicAdd(&s_stat[0], rchk);
-        if (confl) atomicAdd(&s_stat[1], confl);
-        if (wdef) atomicAdd(&s_stat[2], wdef);
-    }
+    const int wid = tid >> 5;
+    if (lane == 0) { s_stat[wid][0] = rchk; s_stat[wid][1] = confl; s_stat[wid][2] = wdef; }
     __syncthreads();
     if (tid == 0) {
-        pc.resolve_checks += s_stat[0];
-        pc.conflicts += s_stat[1];
-        pc.w_def += s_stat[2];
+        for (int w = 0; w < kPWarps; ++w) {
+            pc.resolve_checks += s_stat[w][0];
+            pc.conflicts += s_stat[w][1];
+            pc.w_def += s_stat[w][2];
+        }
     }
     P_TR(4)
     if (tid == 0) {

@@ -1,2 +1,3 @@
-C='[{"cfg":[28,3,"lex"]},{"cfg":[26,4,"gray"]},{"cfg":[24,3,"lex"]}]'
-for S in 65536 262144 524288 1048576; do echo "== submax $S"; GC_SUB_MAX=$S timeout 100 python tools/sweep.py "$C"; done
+C='[{"cfg":[28,3,"lex"]},{"cfg":[26,4,"glex"]},{"cfg":[26,4,"gray"]},{"cfg":[24,3,"lex"]},{"cfg":[24,3,"grlex"]},{"cfg":[24,8,"lex"]},{"cfg":[24,3,"gray"]},{"cfg":[24,3,"glex"]}]'
+timeout 100 python tools/sweep.py "$C"
+GC_DEBUG_PHASES=1 timeout 100 python tools/sweep.py '[{"cfg":[28,3,"lex"]}]' 2>&1 | awk '!seen[$0]++' | grep -v "level  [01]: 0"
