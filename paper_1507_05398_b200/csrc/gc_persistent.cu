@@ -84,6 +84,8 @@ struct PState {
     unsigned long long t_items[kPMaxLevels];   // diagnostics: level start -> last item done (any warp)
     unsigned long long t_item_end[2];          // per-level scratch (alternating slots)
     unsigned long long t_item_max[2];          // per-level scratch: longest warp item
+    unsigned long long item_scan_max[2];       // per-level scratch: most codewords one warp item scanned
+    unsigned long long scan_max_sum[kPMaxLevels];
     unsigned long long t_item_sum[kPMaxLevels];
     unsigned long long t_prefix[kPMaxLevels], n_live[kPMaxLevels], n_items[kPMaxLevels], t_itmax[kPMaxLevels];
     unsigned long long n_overflow, n_seq, n_rounds;
@@ -696,6 +698,7 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                 sc = p_scan<R, MIX>(a.codebook, s_lo, s_hi, cur0, v, m, a.d);
             }
             my_checks += (unsigned long long)sc * R;   // per lane; summed over lanes at the end
+            if (a.timing && (threadIdx.x & 31) == 0) atomicMax(&a.st->item_scan_max[lv.l & 1], (unsigned long long)sc);
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -1312,6 +1315,8 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                 st->t_item_end[l & 1] = 0;
                 timer->item_max[l] += __ldcg(&st->t_item_max[l & 1]);
                 st->t_item_max[l & 1] = 0;
+                st->scan_max_sum[l] += __ldcg(&st->item_scan_max[l & 1]);
+                st->item_scan_max[l & 1] = 0;
                 timer->level[l] += t - tm;
                 timer->items[l] += e > tm ? e - tm : 0;
                 tm = t;
@@ -1638,9 +1643,9 @@ static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a) {
             for (int l = 0; l < kPMaxLevels; ++l)
                 if (full.t_level[l])
                     fprintf(stderr, "[gc]   level %2d: per tile %.1f live candidates, %.1f items; prefix %.2f us, "
-                            "warp item mean %.2f us, longest %.2f us\n", l, full.n_live[l] / T, full.n_items[l] / T,
+                            "warp item mean %.2f us, longest %.2f us, most codewords scanned by one item %.0f\n", l, full.n_live[l] / T, full.n_items[l] / T,
                             full.t_prefix[l] / T / 1e3, full.t_item_sum[l] / (double)std::max(1ull, full.n_items[l]) / 1e3,
-                            full.t_itmax[l] / T / 1e3);
+                            full.t_itmax[l] / T / 1e3, full.scan_max_sum[l] / T);
         }
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }
