@@ -382,11 +382,13 @@ def run_b200(args):
                          "screen_share_of_step": (screen_ms / args.steps) / ms_per_step,
                          "screen_launches_per_step": stats[-1]["screen_launches"],
                          "regime": "latency-bound: the block bound leaves W_exec ~1e-4 of W_def, so a step is "
-                                   "a chain of dependent tiles (levels + grid barriers + in-tile resolve); "
-                                   "frac is the executed-check rate against the check-arithmetic peak"},
+                                   "a chain of dependent tiles (levels + grid barriers + in-tile resolve + "
+                                   "commit token); frac is the executed-check rate against the "
+                                   "check-arithmetic peak"},
             "latency": {"tiles_per_step": stats[-1]["tiles"], "levels_per_step": stats[-1]["phases"],
                         "us_per_tile": 1e3 * ms_per_step / max(1, stats[-1]["tiles"]),
-                        "grid_barriers_per_step": stats[-1]["phases"] + stats[-1]["tiles"]},
+                        "grid_barriers_per_step": stats[-1]["phases"],
+                        "commit_tokens_per_step": stats[-1]["tiles"]},
             "e2e": {"value": e2e_val, "unit": "checks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(sum(s["launches"] for s in stats)),
             "clocks": clocks,
