@@ -28,7 +28,7 @@ int resolve_options(const gc_options *opt, Options *out) {
         }
         if (opt->tile_min) o.tile_min = opt->tile_min;
         if (opt->tile_max) o.tile_max = opt->tile_max;
-        if (opt->window0) o.window0 = opt->window0;
+        if (opt->window0) { o.window0 = opt->window0; o.window0_set = true; }
         if (opt->emulate_ranks) o.emulate_ranks = opt->emulate_ranks;
         o.flags = opt->flags;
         if (opt->window_growth) o.growth = opt->window_growth;

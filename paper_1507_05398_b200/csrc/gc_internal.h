@@ -19,6 +19,7 @@ struct Options {
     uint32_t tile_min = 256;
     uint32_t tile_max = 0;          // 0 = engine default (persistent 4096, launched 65536)
     uint32_t window0 = 4096;
+    bool window0_set = false;       // window0 given by the caller (else engine default)
     uint32_t emulate_ranks = 1;
     uint32_t flags = 0;
     uint32_t growth = 0;            // log2 window growth per level, 0 = engine default (launched

@@ -1534,7 +1534,12 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     a.N = 1ull << r.n;
     a.tile_min = r.opt.tile_min; a.tile_max = r.opt.tile_max ? r.opt.tile_max : kPDefaultTile;
     if (a.tile_min > a.tile_max) a.tile_min = a.tile_max;
-    a.W0 = r.opt.window0;
+    // lexicographic order with the block bound: one level over the whole codebook (its tiles'
+    // candidates are consecutive integers, so a warp's 64 share all but their low 6 bits and the
+    // bound alone prunes the deep part; a separate newest-first level costs more than it saves)
+    const bool lex_single = !r.opt.window0_set && r.ordering == LEX && !r.use_basis && !r.self_orthogonal &&
+                            !(r.opt.flags & GC_FLAG_NO_BLOCK_BOUND);
+    a.W0 = lex_single ? (1u << 24) : r.opt.window0;
     // default window growth: without the block bound x4 per level; with it, two levels (newest
     // W0, then everything) for lex / Gray / B-orderings, where the bound skips almost all of a
     // deep window, and x16 for graded orders, where it skips less and compaction pays
@@ -1552,7 +1557,7 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     // (graded orders, whose deep windows pass more blocks, balance better with more, smaller items:
     // warps claim them dynamically)
     a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP")))
-                       : !a.bound ? 2 : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4 : 1;
+                       : !a.bound ? 2 : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4 : lex_single ? 2 : 1;
     a.sub_max_bound = getenv("GC_SUB_MAX") ? (uint32_t)std::max(64, atoi(getenv("GC_SUB_MAX"))) : 131072u;
     a.partial_s = getenv("GC_PARTIAL_S") ? (uint32_t)std::max(32, atoi(getenv("GC_PARTIAL_S")))
                   : (r.ordering >= GRADED_LEX && !r.use_basis) ? 1024u : 512u;
