@@ -1534,10 +1534,10 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     a.N = 1ull << r.n;
     a.tile_min = r.opt.tile_min; a.tile_max = r.opt.tile_max ? r.opt.tile_max : kPDefaultTile;
     if (a.tile_min > a.tile_max) a.tile_min = a.tile_max;
-    // lexicographic order with the block bound: one level over the whole codebook (its tiles'
+    // lexicographic order, d <= 3, with the block bound: one level over the whole codebook (its tiles
     // candidates are consecutive integers, so a warp's 64 share all but their low 6 bits and the
     // bound alone prunes the deep part; a separate newest-first level costs more than it saves)
-    const bool lex_single = !r.opt.window0_set && r.ordering == LEX && !r.use_basis && !r.self_orthogonal &&
+    const bool lex_single = !r.opt.window0_set && r.ordering == LEX && r.d <= 3 && !r.use_basis && !r.self_orthogonal &&
                             !(r.opt.flags & GC_FLAG_NO_BLOCK_BOUND);
     a.W0 = lex_single ? (1u << 24) : r.opt.window0;
     // default window growth: without the block bound x4 per level; with it, two levels (newest
