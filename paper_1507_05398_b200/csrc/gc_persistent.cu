@@ -5,18 +5,21 @@
 //
 // Per tile of K consecutive ranks [t0, t0+K):
 //   levels l = 0 .. L-1   a1+a2: every candidate against the codebook committed before the
-//                         tile, newest first, in geometrically growing windows
-//                         [M - W0(2^l - 1) - W0 2^l, M - W0(2^l - 1)), the last one down to 0.
-//                         Work items are WARP-granular: (64 candidates, <= kSub codewords);
-//                         codewords are read with warp-uniform 128-bit loads (L1/L2 broadcast),
-//                         XOR + POPC + min per check, warp-vote early exit.  The warp that
-//                         completes a batch's last item pushes the batch's live candidates to
-//                         the next level's list, so no compaction pass/barrier is needed.
-//   grid barrier after each level (the dead bits of level l decide level l+1's list)
-//   resolve (CTA 0)       a3: survivors in rank order; a survivor with no earlier in-tile
-//                         conflict is accepted outright, the others are decided in rank order
-//                         against the accepted ones (PAPER.md:59 inside the tile); a4: append.
-//   grid barrier          the commit is visible to every CTA before the next tile.
+//                         tile, newest first, in growing windows, the last one down to 0
+//                         (lex with d <= 3: one window).  Work items are WARP-granular:
+//                         (64 candidates, one sub-range of the window), claimed from a
+//                         per-CTA counter.  A block of 32 codewords is skipped when its
+//                         bit-consensus bound is >= d; the blocks that pass are staged in
+//                         shared memory and checked (XOR + POPC + min, warp-vote early exit).
+//                         Level 0's window is copied to shared memory once per CTA; deeper
+//                         levels find their live candidates through a per-CTA prefix of
+//                         the tile's dead mask.
+//   grid barrier after each level (the dead bits of level l decide level l+1's live set)
+//   resolve (CTA 0)       a3: survivors in rank order (tiles with more than 512 are cut after
+//                         them); conflict masks, parallel rounds, warp-sequential tail
+//                         (PAPER.md:59 inside the tile); a4: append + block summaries.
+//   commit token          CTA 0 publishes M and the next tile size (release); the others
+//                         wait for it (acquire) -- the commit needs no second barrier.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -115,7 +118,6 @@ struct PArgs {
     int part_mode;
     unsigned long long t_single;
     uint32_t K_single, part_lo, part_len;
-    int vals_valid;                 // a.vals holds every candidate of the tile (else regenerate)
     // SURVEY 8(f) extensions
     int use_basis;                  // B-ordering: rank -> XOR of basis[j] over set bits j
     uint32_t basis[32];
@@ -135,9 +137,7 @@ struct PArgs {
     const OrderTables *tabs;
     uint32_t *vals;                 // [kPMaxTile]
     uint32_t *dead;                 // [kPMaxTile / 32]
-    uint2 *q0, *q1;                 // level lists (ping-pong), [kPMaxTile] each
     uint2 *surv;                    // [kPMaxTile]
-    uint8_t *status;                // [kPMaxTile]
     PState *st;
     unsigned long long *d_count;
     int timing;
@@ -1424,8 +1424,7 @@ __global__ void __launch_bounds__(kPThreads, 1) k_resolve_tile(PArgs a) {
 struct PContext {
     int device = -1, sms = 0;
     uint32_t *vals = nullptr, *dead = nullptr;
-    uint2 *q0 = nullptr, *q1 = nullptr, *surv = nullptr;
-    uint8_t *status = nullptr;
+    uint2 *surv = nullptr;
     uint32_t *bsum = nullptr;       // block-bound summaries: (AND, OR) per block, then per super-block
     size_t bsum_words = 0;          // allocated u32 words
     PState *st = nullptr;
@@ -1457,10 +1456,7 @@ static int p_context(int device, PContext **out) {
         PCK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
         PCK(cudaMalloc(&c->vals, kPMaxTile * 4));
         PCK(cudaMalloc(&c->dead, kPMaxTile / 8));
-        PCK(cudaMalloc(&c->q0, kPMaxTile * sizeof(uint2)));
-        PCK(cudaMalloc(&c->q1, kPMaxTile * sizeof(uint2)));
         PCK(cudaMalloc(&c->surv, kPMaxTile * sizeof(uint2)));
-        PCK(cudaMalloc(&c->status, kPMaxTile));
         PCK(cudaMalloc(&c->st, sizeof(PState)));
         PCK(cudaMalloc(&c->tabs, sizeof(OrderTables)));
         PCK(cudaEventCreate(&c->ev0));
@@ -1548,7 +1544,7 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     a.mix = (r.d >= 2 && r.d <= 4 && !(r.opt.flags & GC_FLAG_POPC_ONLY)) ? (int)r.d : 0;
     a.codebook = r.d_codebook; a.capacity = r.capacity;
     a.tabs = cx->tabs; a.vals = cx->vals; a.dead = cx->dead;
-    a.q0 = cx->q0; a.q1 = cx->q1; a.surv = cx->surv; a.status = cx->status;
+    a.surv = cx->surv;
     a.st = cx->st; a.d_count = (unsigned long long *)r.d_count;
     a.timing = getenv("GC_DEBUG_PHASES") != nullptr;
     a.bound = !r.self_orthogonal && !(r.opt.flags & GC_FLAG_NO_BLOCK_BOUND);
@@ -1581,7 +1577,6 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     }
     if (a.mix && r.self_orthogonal) a.mix = 0;
     a.part_mode = 0;
-    a.vals_valid = 1;
     a.t_single = 0; a.K_single = 0; a.part_lo = 0; a.part_len = 0;
     *pa = a;
     return GC_OK;
@@ -1676,7 +1671,6 @@ int persistent_run_partitioned(const RunArgs &r) {
     const unsigned G = r.world > 1 ? (unsigned)r.world : r.opt.emulate_ranks;
     const unsigned parts_local = r.world > 1 ? 1u : G;
     a.part_mode = 1;
-    a.vals_valid = 0;
     a.chunk = 4096u;
     const uint32_t tile_max = r.opt.tile_max ? r.opt.tile_max : 16384u;
     const size_t smem = p_dyn_smem(a.chunk);
