@@ -114,6 +114,7 @@ struct PArgs {
     uint32_t target_accepted;       // adaptive tiles grow toward ~this many accepted words per tile
     uint32_t sub_max_bound;         // longest window sub-range per warp item with the block bound
     uint32_t partial_s;             // persistent engine: a tile with more survivors is cut after this many
+    uint32_t geo_head;              // first (newest) window sub-range of a level; 0 = uniform sub-ranges
     // partition mode (multi-GPU / emulated ranks): one tile's screen over one candidate range
     int part_mode;
     unsigned long long t_single;
@@ -572,6 +573,8 @@ struct PLevel {
     int l;
     uint32_t n_l, B, nsub;
     long long hi, lo, sub;
+    long long head;          // block bound: the first J0 sub-ranges (newest) are head, 2 head, 4 head,
+    int J0;                  // ... < sub -- the newest words pass the bound most, so they are split finer
     unsigned long long t0;
     const uint32_t *s_pre;   // level >= 1: exclusive prefix of live candidates per mask word (smem)
     const uint32_t *s_live;  // level >= 1: live bits per mask word (smem)
@@ -607,8 +610,11 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                                        unsigned long long &my_checks) {
     const int lane = threadIdx.x & 31;
     const uint32_t j = (uint32_t)(it / lv.B), b = (uint32_t)(it % lv.B);
-    const long long s_hi = lv.hi - (long long)j * lv.sub;            // j = 0: newest
-    const long long s_lo = max(lv.lo, s_hi - lv.sub);
+    long long v0, vlen;                                               // j = 0: newest
+    if ((int)j < lv.J0) { v0 = lv.head * ((1ll << j) - 1); vlen = lv.head << j; }
+    else { v0 = lv.head * ((1ll << lv.J0) - 1) + (long long)(j - lv.J0) * lv.sub; vlen = lv.sub; }
+    const long long s_hi = lv.hi - v0;
+    const long long s_lo = max(lv.lo, s_hi - vlen);
     // first codeword block in flight while the candidates are fetched
     const uint32_t cur0 = (!a.bound || MIX == 1) && (s_hi - 1 - lane >= s_lo) ? __ldcg(a.codebook + s_hi - 1 - lane) : 0u;
     uint32_t v[R], m[R], idx[R];
@@ -1226,7 +1232,8 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             const uint32_t B = (n_l + batch - 1) / batch;
             // sub-ranges of the window, newest first, sized so the level has ~4 items per warp
             const long long wlen = hi - lo;
-            long long sub = 0;
+            long long sub = 0, head = 0;
+            int J0 = 0;
             uint32_t nsub = 0;
             if (wlen > 0 && B > 0) {
                 const long long want = ((long long)nwarps * a.items_per_warp + B - 1) / B;   // sub-ranges wanted
@@ -1234,12 +1241,19 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
                 sub = (sub + 31) & ~31ll;
                 sub = max(sub, (long long)kPSubMin);
                 sub = min(sub, a.bound ? (long long)a.sub_max_bound : (long long)kPSubMax);
-                nsub = (uint32_t)((wlen + sub - 1) / sub);
+                head = sub;
+                J0 = 0;
+                if (a.bound && a.geo_head > 0 && sub > (long long)a.geo_head) {
+                    head = a.geo_head;
+                    while ((head << (J0 + 1)) <= sub && head * ((1ll << (J0 + 1)) - 1) < wlen) ++J0;
+                }
+                const long long headlen = head * ((1ll << J0) - 1);
+                nsub = (uint32_t)J0 + (wlen > headlen ? (uint32_t)((wlen - headlen + sub - 1) / sub) : 0u);
             }
             const unsigned long long checks_before = my_checks;
             PLevel lv;
             lv.l = l; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
-            lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0;
+            lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0; lv.head = head; lv.J0 = J0;
             lv.s_pre = s_pre; lv.s_live = s_live; lv.words = pwords; lv.basis = s_basis; lv.stage = reinterpret_cast<uint32_t *>(p_dyn); lv.c_lo = c_lo; lv.w_base = w_lo * 32;
             lv.win = nullptr; lv.wsum = nullptr; lv.win_lo = 0;
             if (l == 0 && a.bound && !a.so && hi > lo && hi - (lo & ~31ll) <= (long long)kPWinWords) {
@@ -1553,8 +1567,9 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     // (graded orders, whose deep windows pass more blocks, balance better with more, smaller items:
     // warps claim them dynamically)
     a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP")))
-                       : !a.bound ? 2 : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4 : lex_single ? 2 : 1;
+                       : !a.bound ? 2 : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4 : 1;
     a.sub_max_bound = getenv("GC_SUB_MAX") ? (uint32_t)std::max(64, atoi(getenv("GC_SUB_MAX"))) : 131072u;
+    a.geo_head = getenv("GC_GEO_HEAD") ? (uint32_t)std::max(0, atoi(getenv("GC_GEO_HEAD"))) : 16384u;
     a.partial_s = getenv("GC_PARTIAL_S") ? (uint32_t)std::max(32, atoi(getenv("GC_PARTIAL_S")))
                   : (r.ordering >= GRADED_LEX && !r.use_basis) ? 1024u : 512u;
     a.target_accepted = getenv("GC_TARGET_ACCEPTED") ? (uint32_t)std::max(1, atoi(getenv("GC_TARGET_ACCEPTED")))

@@ -1,1 +1,2 @@
-timeout 100 python tools/sweep.py '[{"cfg":[26,4,"lex"]},{"cfg":[24,5,"lex"]},{"cfg":[28,3,"lex"]},{"cfg":[24,2,"lex"]},{"cfg":[24,2,"lex"],"opts":{"window0":4096}}]'
+C='[{"cfg":[28,3,"lex"]},{"cfg":[26,4,"glex"]},{"cfg":[26,4,"gray"]},{"cfg":[26,4,"lex"]},{"cfg":[24,3,"lex"]},{"cfg":[24,3,"grlex"]},{"cfg":[24,3,"gray"]},{"cfg":[24,3,"glex"]},{"cfg":[24,8,"lex"]}]'
+timeout 100 python tools/sweep.py "$C"
