@@ -115,6 +115,8 @@ struct PArgs {
     uint32_t sub_max_bound;         // longest window sub-range per warp item with the block bound
     uint32_t partial_s;             // persistent engine: a tile with more survivors is cut after this many
     uint32_t geo_head;              // first (newest) window sub-range of a level; 0 = uniform sub-ranges
+    uint32_t nsup_smem;             // super-block summaries [0, nsup_smem) mirrored in every CTA's shared
+                                    // memory (persistent mode; refreshed as commits change them)
     // partition mode (multi-GPU / emulated ranks): one tile's screen over one candidate range
     int part_mode;
     unsigned long long t_single;
@@ -467,7 +469,8 @@ __device__ __forceinline__ uint32_t p_scan_window(const PArgs &a, const uint32_t
 //   3. the passing blocks are queued; every 32 of them are staged and checked (p_scan_list).
 template <int R, int MIX>
 __device__ __forceinline__ uint32_t p_scan_bound(const PArgs &a, long long lo, long long hi, uint32_t cA, uint32_t cO,
-                                                 const uint32_t (&v)[R], uint32_t (&m)[R], uint32_t *stage) {
+                                                 const uint32_t (&v)[R], uint32_t (&m)[R], uint32_t *stage,
+                                                 const uint2 *s_sup) {
     const int lane = threadIdx.x & 31;
     uint32_t scanned = 0;
     if (hi - lo <= 4096) {
@@ -482,7 +485,7 @@ __device__ __forceinline__ uint32_t p_scan_bound(const PArgs &a, long long lo, l
         const long long sb = sg - lane;
         bool pass = false;
         if (sb >= sb_lo) {
-            const uint2 ss = __ldcg(a.ssum + sb);
+            const uint2 ss = sb < (long long)a.nsup_smem ? s_sup[sb] : __ldcg(a.ssum + sb);
             pass = p_lb(ss.x, ss.y, cA, cO, a.nmask) < a.d;
         }
         uint32_t smask = __ballot_sync(0xffffffffu, pass);
@@ -581,6 +584,7 @@ struct PLevel {
     uint32_t words;
     const uint32_t *basis;   // B-ordering basis (smem)
     uint32_t *stage;         // block-bound staging, kPStageWords per warp (smem; aliases the resolve scratch)
+    const uint2 *s_sup;      // shared-memory mirror of the first a.nsup_smem super-block summaries
     const uint32_t *win;     // level 0 with the block bound: the whole window, copied to shared memory
     const uint2 *wsum;       //   once per CTA (words [win_lo, hi), win_lo = lo & ~31) and its block summaries
     long long win_lo;
@@ -669,7 +673,7 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                 uint32_t *stg = lv.stage + (threadIdx.x >> 5) * kPWarpStage;
                 auto scan = [&](uint32_t sA, uint32_t sO, uint32_t (&mm)[R]) {
                     return lv.win ? p_scan_window<R, MIX>(a, lv.win, lv.wsum, lv.win_lo, s_lo, s_hi, sA, sO, v, mm)
-                                  : p_scan_bound<R, MIX>(a, s_lo, s_hi, sA, sO, v, mm, stg);
+                                  : p_scan_bound<R, MIX>(a, s_lo, s_hi, sA, sO, v, mm, stg, lv.s_sup);
                 };
                 const uint32_t vary = cO & ~cA;            // bits on which the live candidates differ
                 // (not for graded orders: a weight class in colex order varies many bits by
@@ -1143,6 +1147,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     uint16_t *s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 12);
     uint32_t *s_pre = reinterpret_cast<uint32_t *>(p_dyn + p_scratch_smem(kPChunk));
     uint32_t *s_live = s_pre + kPMaxTile / 32 + 4;
+    uint2 *s_sup = reinterpret_cast<uint2 *>(p_dyn + p_dyn_smem(kPChunk));     // [a.nsup_smem]
     __shared__ uint32_t s_basis[32];
     __shared__ unsigned int s_claim;            // per-level item claims of this CTA
     PState *st = a.st;
@@ -1171,6 +1176,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     // by the commit token (no barrier and no load of M / K_next after a resolve)
     unsigned long long curM = __ldcg(&st->M);
     uint32_t curK = __ldcg(&st->K_next);
+    unsigned long long supM = 0;            // the shared super-block mirror is final below supM
     unsigned long long tile_no = 0;
     __shared__ unsigned long long s_tok;
     __shared__ uint32_t s_kused;
@@ -1178,6 +1184,14 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
     while (t0 < a.t_end) {
         const unsigned long long M = curM;
         uint32_t K = a.part_mode ? a.K_single : curK;
+        if (a.nsup_smem) {
+            // refresh the mirrored super-block summaries the last commits changed (the partial one
+            // and the new ones); every level syncs the CTA before its items read them
+            const long long s0 = (long long)(supM >> 10);
+            const long long s1 = min((long long)a.nsup_smem, (long long)((M + 1023) >> 10));
+            for (long long q = s0 + threadIdx.x; q < s1; q += blockDim.x) s_sup[q] = __ldcg(a.ssum + q);
+            supM = M;
+        }
         if ((unsigned long long)K > a.t_end - t0) K = (uint32_t)(a.t_end - t0);
         // candidate range screened by this launch: the tile, or one rank's partition of it
         const uint32_t c_lo = a.part_mode ? min(a.part_lo, K) : 0u;
@@ -1254,7 +1268,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_construct(PArgs a) {
             PLevel lv;
             lv.l = l; lv.n_l = n_l; lv.B = B; lv.nsub = nsub;
             lv.hi = hi; lv.lo = lo; lv.sub = sub; lv.t0 = t0; lv.head = head; lv.J0 = J0;
-            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = pwords; lv.basis = s_basis; lv.stage = reinterpret_cast<uint32_t *>(p_dyn); lv.c_lo = c_lo; lv.w_base = w_lo * 32;
+            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = pwords; lv.basis = s_basis; lv.stage = reinterpret_cast<uint32_t *>(p_dyn); lv.s_sup = s_sup; lv.c_lo = c_lo; lv.w_base = w_lo * 32;
             lv.win = nullptr; lv.wsum = nullptr; lv.win_lo = 0;
             if (l == 0 && a.bound && !a.so && hi > lo && hi - (lo & ~31ll) <= (long long)kPWinWords) {
                 // level 0 with the block bound: every item scans part of the same small window,
@@ -1569,6 +1583,7 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP")))
                        : !a.bound ? 2 : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4 : 1;
     a.sub_max_bound = getenv("GC_SUB_MAX") ? (uint32_t)std::max(64, atoi(getenv("GC_SUB_MAX"))) : 131072u;
+    a.nsup_smem = 0;                // set by the launcher when shared memory has room
     a.geo_head = getenv("GC_GEO_HEAD") ? (uint32_t)std::max(0, atoi(getenv("GC_GEO_HEAD"))) : 16384u;
     a.partial_s = getenv("GC_PARTIAL_S") ? (uint32_t)std::max(32, atoi(getenv("GC_PARTIAL_S")))
                   : (r.ordering >= GRADED_LEX && !r.use_basis) ? 1024u : 512u;
@@ -1604,8 +1619,20 @@ static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a) {
     const char *ev = getenv("GC_PERSIST_CTAS");
     const int ctas = (ev && atoi(ev) == 2) ? 2 : 1;
     const void *kfn = ctas == 2 ? (const void *)k_construct<2> : (const void *)k_construct<1>;
-    a.chunk = ctas == 2 ? 2048u : 4096u;
-    const size_t smem = p_dyn_smem(a.chunk);
+    a.chunk = 2048u;            // partial tiles keep a persistent tile's survivors <= 1024
+    size_t smem = p_dyn_smem(a.chunk);
+    // mirror as many super-block summaries in shared memory as fit (one CTA per SM)
+    a.nsup_smem = 0;
+    if (ctas == 1 && a.bound && !getenv("GC_NO_SUP_SMEM")) {
+        cudaFuncAttributes fa;
+        int optin = 0;
+        PCK(cudaFuncGetAttributes(&fa, kfn));
+        PCK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cx->device));
+        const long long room = (long long)optin - (long long)fa.sharedSizeBytes - (long long)smem;
+        const unsigned long long need = (r.capacity + 1023) / 1024 + 1;
+        if (room >= 8) a.nsup_smem = (uint32_t)std::min<unsigned long long>(need, (unsigned long long)(room / 8));
+        smem += (size_t)a.nsup_smem * 8;
+    }
     PCK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     PCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kPThreads, smem));
     if (per_sm < ctas) { set_error("k_construct cannot be resident"); return GC_ECUDA; }
