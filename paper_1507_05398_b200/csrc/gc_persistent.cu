@@ -57,6 +57,7 @@ constexpr uint32_t kPWinWords = 16384 + 32;     // level-0 window copied to shar
 constexpr int kPSplitBits = 12;                 // a warp's live candidates differing in more bits are
                                                 // screened as two halves (block bound, p_item)
 constexpr uint32_t kPOvf = 1024;
+constexpr uint32_t kPChunkMaxGroups = 4096 / 32;  // groups of 32 survivors in the largest resolve chunk
 constexpr uint32_t kPResolveTmp = 2048;         // k_resolve_tile: staging words after the scratch                // overflow survivors decided warp-parallel (per chunk)
 constexpr uint32_t kPOvfMark = 0xffffffffu;     // s_cnt of a listed overflow survivor
 // resolve scratch: s_val (4 B) + s_idx (2 B) + s_status (1 B) + pad (1 B) + s_cnt (4 B) + s_adj (2 B x kPAdj)
@@ -855,6 +856,7 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
     __shared__ uint16_t s_ovf[kPOvf];
     __shared__ uint32_t s_novf;
     __shared__ uint32_t s_wmin[33];          // graded orders: first tile position of each weight
+    __shared__ uint32_t s_gA[kPChunkMaxGroups], s_gO[kPChunkMaxGroups];   // survivor group consensus
     if (tid < 33) s_wmin[tid] = 0xffffffffu;
     unsigned long long rchk = 0, confl = 0, wdef = 0;
     const unsigned long long M0 = pc.M;
@@ -874,12 +876,24 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         // survivors): a bit mask of the conflicting ones, appended to j's adjacency list
         // (s_adj, up to kPAdj entries, any order; s_cnt[j] > kPAdj marks an overflow)
         const uint32_t ng = (Sc + 31) / 32;
-        auto units = [&](auto so_tag) {
+        // group consensus (AND / OR of 32 survivors) for the bound between two groups
+        for (uint32_t g = tid >> 5; g < ng; g += blockDim.x >> 5) {
+            const uint32_t k = 32 * g + lane;
+            const uint32_t x = k < Sc ? s_val[k] : 0u;
+            const uint32_t gA = __reduce_and_sync(0xffffffffu, k < Sc ? x : ~0u);
+            const uint32_t gO = __reduce_or_sync(0xffffffffu, x);
+            if (lane == 0) { s_gA[g] = gA; s_gO[g] = gO; }
+        }
+        __syncthreads();
+        // MIX (2..4, distance-only problems): odd columns use the ALU bit-clearing form of the
+        // same predicate, so the XU (POPC) and ALU pipes share the one SM's work
+        auto units = [&](auto so_tag, auto mix_tag) {
             constexpr bool SO = decltype(so_tag)::value;
-            auto cf = [&](uint32_t u, uint32_t w) {
+            constexpr int MIXC = decltype(mix_tag)::value;
+            auto cf = [&](uint32_t u, uint32_t w, int t) {
+                if (MIXC >= 2 && (t & 1)) return p_clear_low<MIXC>(u ^ w) == 0u;
                 return (uint32_t)__popc(u ^ w) < a.d || (SO && (__popc(u & w) & 1));
-            };
-            // warp task p = block pair (jb, kg <= jb): lane t holds survivor 32 jb + t, the 32
+            };            // warp task p = block pair (jb, kg <= jb): lane t holds survivor 32 jb + t, the 32
             // survivors of group kg are broadcast by shuffles (no division, no idle lanes but on
             // the diagonal)
             const uint32_t ntask = ng * (ng + 1) / 2;
@@ -889,10 +903,13 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
                 while (jb * (jb + 1) / 2 > p) --jb;
                 const uint32_t kg = p - jb * (jb + 1) / 2;
                 const uint32_t j = 32 * jb + lane, k = 32 * kg + lane;
+                // two groups whose consensus bound is >= d hold no conflicting pair (not for the
+                // orthogonality constraint)
+                if (!SO && p_lb(s_gA[jb], s_gO[jb], s_gA[kg], s_gO[kg], a.nmask) >= a.d) continue;
                 const uint32_t vj = j < Sc ? s_val[j] : 0u, vk = k < Sc ? s_val[k] : 0u;
                 uint32_t mask = 0;
 #pragma unroll
-                for (int t = 0; t < 32; ++t) mask |= (uint32_t)cf(vj, __shfl_sync(0xffffffffu, vk, t)) << t;
+                for (int t = 0; t < 32; ++t) mask |= (uint32_t)cf(vj, __shfl_sync(0xffffffffu, vk, t), t) << t;
                 const uint32_t kmax = min(j, Sc);                 // earlier survivors only
                 const uint32_t lim = kmax > 32 * kg ? min(32u, kmax - 32 * kg) : 0u;
                 mask &= lim >= 32 ? 0xffffffffu : ((1u << lim) - 1u);
@@ -908,8 +925,11 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
                 }
             }
         };
-        if (a.so) units(std::true_type{});
-        else units(std::false_type{});
+        if (a.so) units(std::true_type{}, std::integral_constant<int, 0>{});
+        else if (a.mix == 2) units(std::false_type{}, std::integral_constant<int, 2>{});
+        else if (a.mix == 3) units(std::false_type{}, std::integral_constant<int, 3>{});
+        else if (a.mix == 4) units(std::false_type{}, std::integral_constant<int, 4>{});
+        else units(std::false_type{}, std::integral_constant<int, 0>{});
         __syncthreads();
         // status: 1 = accepted, 0 = rejected, 2 = undecided.  A survivor conflicting with a word
         // accepted in an earlier chunk of this tile is rejected outright (multi-chunk tiles only).
