@@ -220,7 +220,7 @@ def run_reference(args):
         "value": val, "unit": "checks/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (the whole space F_2^n, no dataset)",
-        "config": {"workload": f"n={n},d={d},{o}", "sample": sample},
+        "config": {"workload": args.workload, "sample": sample},
         "cpu_baseline": {"value": val, "unit": "checks/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": val, "unit": "checks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
