@@ -116,6 +116,7 @@ struct PArgs {
     uint32_t sub_max_bound;         // longest window sub-range per warp item with the block bound
     uint32_t partial_s;             // persistent engine: a tile with more survivors is cut after this many
     uint32_t geo_head;              // first (newest) window sub-range of a level; 0 = uniform sub-ranges
+    int split_bits;                 // a warp whose live candidates vary in more bits screens two halves
     uint32_t nsup_smem;             // super-block summaries [0, nsup_smem) mirrored in every CTA's shared
                                     // memory (persistent mode; refreshed as commits change them)
     // partition mode (multi-GPU / emulated ranks): one tile's screen over one candidate range
@@ -679,7 +680,7 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                 const uint32_t vary = cO & ~cA;            // bits on which the live candidates differ
                 // (not for graded orders: a weight class in colex order varies many bits by
                 // nature, and the weight bound already cuts their windows)
-                if (__popc(vary) <= kPSplitBits || (a.ord >= GRADED_LEX && !a.use_basis)) {
+                if (__popc(vary) <= a.split_bits || (a.ord >= GRADED_LEX && !a.use_basis)) {
                     sc = scan(cA, cO, m);
                 } else {
                     // weak consensus (typically a batch straddling a carry of a high bit): scan
@@ -1604,6 +1605,7 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
                        : !a.bound ? 2 : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4 : 1;
     a.sub_max_bound = getenv("GC_SUB_MAX") ? (uint32_t)std::max(64, atoi(getenv("GC_SUB_MAX"))) : 131072u;
     a.nsup_smem = 0;                // set by the launcher when shared memory has room
+    a.split_bits = getenv("GC_SPLIT_BITS") ? atoi(getenv("GC_SPLIT_BITS")) : lex_single ? kPSplitBits - 2 : kPSplitBits;
     a.geo_head = getenv("GC_GEO_HEAD") ? (uint32_t)std::max(0, atoi(getenv("GC_GEO_HEAD"))) : 16384u;
     a.partial_s = getenv("GC_PARTIAL_S") ? (uint32_t)std::max(32, atoi(getenv("GC_PARTIAL_S")))
                   : (r.ordering >= GRADED_LEX && !r.use_basis) ? 1024u : 512u;
