@@ -70,14 +70,18 @@ typedef struct gc_options {
     uint32_t struct_size;
     uint32_t tile_min;       /* smallest candidate tile K (power of 2, >= 32), default 256              */
     uint32_t tile_max;       /* largest candidate tile K (power of 2, <= 2^20), default 65536; the
-                                persistent kernel (tiles <= 65536) sizes tiles adaptively for ~128
-                                accepted words per tile                                          */
-    uint32_t window0;        /* first newest-first codebook window (power of 2), default 4096           */
+                                persistent kernel (tiles <= 65536) sizes tiles adaptively for
+                                ~384 accepted words per tile (768 for graded orders) and cuts a
+                                tile after 512 survivors (1024 graded); neither changes the code  */
+    uint32_t window0;        /* first newest-first codebook window (power of 2, <= 2^24); default: 4096,
+                                and for the persistent engine with the block bound in lexicographic
+                                order with d <= 3 the whole codebook (one screening level)       */
     uint32_t emulate_ranks;  /* >1: split every tile's candidates into this many partitions on ONE GPU,
                                 exactly as gc_generate_rank splits them across GPUs (testing), default 1 */
     uint32_t flags;          /* GC_FLAG_* below                                                          */
     uint32_t window_growth;  /* log2 of the factor by which each newest-first window grows over the
-                                previous one (1 = doubling ... 4 = x16), default 2                         */
+                                previous one (1 = doubling ... 12 = x4096); default 2, and for the
+                                persistent engine with the block bound 4 (graded orders) or 12      */
 } gc_options;
 
 #define GC_FLAG_NO_EARLY_EXIT  0x1u  /* screen every candidate against the whole codebook, one phase     */
