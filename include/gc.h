@@ -71,7 +71,7 @@ typedef struct gc_options {
     uint32_t tile_min;       /* smallest candidate tile K (power of 2, >= 32), default 256              */
     uint32_t tile_max;       /* largest candidate tile K (power of 2, <= 2^20), default 65536; the
                                 persistent kernel (tiles <= 65536) sizes tiles adaptively for
-                                ~384 accepted words per tile (768 for graded orders) and cuts a
+                                ~384 accepted words per tile (768 Gray, 1536 graded) and cuts a
                                 tile after 512 survivors (1024 graded); neither changes the code  */
     uint32_t window0;        /* first newest-first codebook window (power of 2, <= 2^24); default: 4096,
                                 and for the persistent engine with the block bound in lexicographic

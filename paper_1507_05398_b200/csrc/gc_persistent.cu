@@ -47,7 +47,8 @@ constexpr uint32_t kPMaxTile = 1u << 16;    // largest tile (tile indices fit in
 // survivors resolved per chunk (shared memory): 4096 with one CTA per SM, 2048 with two
 constexpr uint32_t kPMaxBatches = kPMaxTile / 32;
 constexpr uint32_t kPTargetAccepted = 384;  // adaptive tiles grow up to ~2x this many accepted words
-                                            // (graded orders: twice that)
+                                            // (Gray: twice that, graded orders: four times;
+                                            // tools/sweep_knobs2.sh, profiles/r01j_knob_sweep.md)
 constexpr uint32_t kPMaxPredictedSurvivors = 1024;
 constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
 constexpr uint32_t kPStageWords = 32 * 32;      // per-warp stage: 32 blocks of 32 codewords (4 KiB)
@@ -1610,7 +1611,9 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     a.partial_s = getenv("GC_PARTIAL_S") ? (uint32_t)std::max(32, atoi(getenv("GC_PARTIAL_S")))
                   : (r.ordering >= GRADED_LEX && !r.use_basis) ? 1024u : 512u;
     a.target_accepted = getenv("GC_TARGET_ACCEPTED") ? (uint32_t)std::max(1, atoi(getenv("GC_TARGET_ACCEPTED")))
-                        : (r.ordering >= GRADED_LEX && !r.use_basis) ? 2 * kPTargetAccepted : kPTargetAccepted;
+                        : r.use_basis ? kPTargetAccepted
+                        : r.ordering >= GRADED_LEX ? 4 * kPTargetAccepted
+                        : r.ordering == GRAY ? 2 * kPTargetAccepted : kPTargetAccepted;
     a.use_basis = r.use_basis;
     for (int i = 0; i < 32; ++i) a.basis[i] = r.basis[i];
     a.so = r.self_orthogonal;
