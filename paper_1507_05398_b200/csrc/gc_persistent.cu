@@ -1604,10 +1604,10 @@ static int p_setup(const RunArgs &r, PContext **pcx, PArgs *pa) {
     // warps claim them dynamically)
     a.items_per_warp = getenv("GC_ITEMS_PER_WARP") ? std::max(1, atoi(getenv("GC_ITEMS_PER_WARP")))
                        : !a.bound ? 2 : (r.ordering >= GRADED_LEX && !r.use_basis) ? 4 : 1;
-    a.sub_max_bound = getenv("GC_SUB_MAX") ? (uint32_t)std::max(64, atoi(getenv("GC_SUB_MAX"))) : 131072u;
+    a.sub_max_bound = getenv("GC_SUB_MAX") ? (uint32_t)std::max(64, atoi(getenv("GC_SUB_MAX"))) : 262144u;
     a.nsup_smem = 0;                // set by the launcher when shared memory has room
     a.split_bits = getenv("GC_SPLIT_BITS") ? atoi(getenv("GC_SPLIT_BITS")) : lex_single ? kPSplitBits - 2 : kPSplitBits;
-    a.geo_head = getenv("GC_GEO_HEAD") ? (uint32_t)std::max(0, atoi(getenv("GC_GEO_HEAD"))) : 16384u;
+    a.geo_head = getenv("GC_GEO_HEAD") ? (uint32_t)std::max(0, atoi(getenv("GC_GEO_HEAD"))) : 8192u;
     a.partial_s = getenv("GC_PARTIAL_S") ? (uint32_t)std::max(32, atoi(getenv("GC_PARTIAL_S")))
                   : (r.ordering >= GRADED_LEX && !r.use_basis) ? 1024u : 512u;
     a.target_accepted = getenv("GC_TARGET_ACCEPTED") ? (uint32_t)std::max(1, atoi(getenv("GC_TARGET_ACCEPTED")))
