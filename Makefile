@@ -16,13 +16,16 @@ $(SRC)/gc_engine.o: $(SRC)/gc_engine.cu $(SRC)/gc_order.cuh $(SRC)/gc_internal.h
 $(SRC)/gc_abi.o: $(SRC)/gc_abi.cpp $(SRC)/gc_internal.h include/gc.h
 	$(NVCC) $(ARCH) -O2 -std=c++17 -Xcompiler -fPIC,-Wall -x cu -c $< -o $@
 
-$(SRC)/gc_persistent.o: $(SRC)/gc_persistent.cu $(SRC)/gc_order.cuh $(SRC)/gc_internal.h include/gc.h
+$(SRC)/gc_persistent.o: $(SRC)/gc_persistent.cu $(SRC)/gc_screen.cuh $(SRC)/gc_order.cuh $(SRC)/gc_internal.h include/gc.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_persistent.ptxas.log || (cat $(SRC)/gc_persistent.ptxas.log; false)
+
+$(SRC)/gc_pipeline.o: $(SRC)/gc_pipeline.cu $(SRC)/gc_screen.cuh $(SRC)/gc_order.cuh $(SRC)/gc_internal.h include/gc.h
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_pipeline.ptxas.log || (cat $(SRC)/gc_pipeline.ptxas.log; false)
 
 $(SRC)/gc_analysis.o: $(SRC)/gc_analysis.cu $(SRC)/gc_internal.h include/gc.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_analysis.ptxas.log || (cat $(SRC)/gc_analysis.ptxas.log; false)
 
-$(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o $(SRC)/gc_persistent.o $(SRC)/gc_analysis.o
+$(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o $(SRC)/gc_persistent.o $(SRC)/gc_pipeline.o $(SRC)/gc_analysis.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl -lpthread
 
 $(ORACLE): oracle/greedy_oracle.c

@@ -81,7 +81,27 @@ typedef struct gc_options {
     uint32_t flags;          /* GC_FLAG_* below                                                          */
     uint32_t window_growth;  /* log2 of the factor by which each newest-first window grows over the
                                 previous one (1 = doubling ... 12 = x4096); default 2, and for the
-                                persistent engine with the block bound 4 (graded orders) or 12      */
+                                persistent engines with the block bound 4 (graded orders) or 12     */
+    /* persistent engines (development / tuning knobs; 0 = default, none changes the code): */
+    uint32_t pipeline_depth; /* pipelined engine: tile i is screened against the codebook committed
+                                after tile i - depth, so `depth` tiles are screened while one is
+                                resolved; 1..16, default 4                                         */
+    uint32_t target_accepted;/* adaptive tiles grow toward ~this many accepted words per tile
+                                (default 384; Gray 768, graded orders 1536)                        */
+    uint32_t items_per_warp; /* screen work items per warp and level (default 1; graded orders 4;
+                                2 without the block bound)                                         */
+    uint32_t sub_max;        /* longest codeword sub-range of one work item with the block bound,
+                                >= 64 (default 262144)                                             */
+    uint32_t geo_head;       /* first (newest) sub-range of a level with the block bound; the next
+                                ones double up to sub_max (default 8192)                           */
+    uint32_t split_bits;     /* a warp whose live candidates differ in more bits screens them as two
+                                halves (default 10 for the one-level lexicographic schedule, else 12) */
+    uint32_t partial_s;      /* tile-barrier engine: a tile is cut after this many survivors, >= 32
+                                (default 512; graded orders 1024)                                  */
+    uint32_t grid_ctas;      /* CTAs of the persistent kernel (default one per SM; the pipelined
+                                engine uses >= 2: one resolves, the others screen)                 */
+    uint32_t plan_warps;     /* pipelined engine: warps a level's work items are planned for
+                                (default: screening warps / pipeline_depth)                        */
 } gc_options;
 
 #define GC_FLAG_NO_EARLY_EXIT  0x1u  /* screen every candidate against the whole codebook, one phase     */
@@ -100,6 +120,11 @@ typedef struct gc_options {
                                         popc((AND_blk & ~OR_batch) | (AND_batch & ~OR_blk)) -- positions
                                         where every codeword of the block differs from every live
                                         candidate of the warp -- is already >= d; exact)            */
+#define GC_FLAG_TILE_BARRIERS  0x100u /* the round-1 tile-synchronous persistent kernel (every CTA screens
+                                        one tile, grid barrier, CTA 0 resolves while the rest wait)
+                                        instead of the pipelined one (testing / comparison)          */
+#define GC_FLAG_DEBUG_PHASES   0x200u /* tile-barrier engine: per-phase timing and counters on stderr     */
+#define GC_FLAG_NO_SUP_SMEM    0x400u /* do not mirror the super-block summaries in shared memory          */
 #define GC_FLAG_KERNEL_TIMING  0x8u  /* bracket every screen launch with CUDA events on the launching
                                         stream; fills gc_stats.screen_ms (benchmarking)               */
 
@@ -121,6 +146,12 @@ typedef struct gc_stats {
     uint64_t launches;       /* kernels this call launched                                            */
     uint64_t screen_launches;/* of which screen kernels (the dominant kernel)                         */
     double screen_ms;        /* summed device time of the screen launches (GC_FLAG_KERNEL_TIMING)     */
+    uint64_t bound_tests;    /* block / super-block summary tests of the block bound (lane evaluations;
+                                each covers 32 or 1024 codewords against a warp's candidates)        */
+    double resolve_wait_ms;  /* pipelined engine: time the resolving CTA waited for screens          */
+    double resolve_busy_ms;  /* pipelined engine: time it spent resolving and committing             */
+    uint32_t pipeline_depth; /* pipelined engine: tiles in flight (0: another engine ran)             */
+    uint32_t reserved;
 } gc_stats;
 
 /* ------------------------------------------------------------------ generate */
@@ -145,8 +176,9 @@ int gc_generate_ex(uint32_t n, uint32_t d, gc_ordering ordering, const gc_option
  * enqueued (results valid when the stream reaches this point; device scratch stays owned
  * by the library and is reused by the next call on this device, which must be ordered
  * after this one -- e.g. the same stream).  With stats != NULL the call synchronises the
- * stream and fills *stats.  If M would exceed capacity the device error flag is set and a
- * later synchronising call reports GC_ENOSPC.  capacity >= gc_capacity_bound(n, d) is safe. */
+ * stream and fills *stats.  If M would exceed capacity, *d_count receives capacity + 1 (a value
+ * above capacity: the code is incomplete) and, with stats != NULL, the call returns GC_ENOSPC.
+ * capacity >= gc_capacity_bound(n, d) is safe.  d_codebook must be 16-byte aligned (GC_EINVAL). */
 int gc_generate_device(uint32_t n, uint32_t d, gc_ordering ordering, const gc_options *opt,
                        uint32_t *d_codebook, uint64_t capacity, uint64_t *d_count,
                        void *stream, gc_stats *stats);

@@ -19,6 +19,9 @@ from ._binding import (  # noqa: F401
     GC_FLAG_NO_WEIGHT_BOUND,
     GC_FLAG_POPC_ONLY,
     GC_FLAG_SYNC_TILES,
+    GC_FLAG_TILE_BARRIERS,
+    GC_FLAG_DEBUG_PHASES,
+    GC_FLAG_NO_SUP_SMEM,
     GC_B_ORDERING,
     GC_GRADED_LEX,
     GC_GRADED_REVLEX,

@@ -27,6 +27,9 @@ GC_FLAG_LAUNCHED_TILES = 0x10
 GC_FLAG_POPC_ONLY = 0x20
 GC_FLAG_NO_WEIGHT_BOUND = 0x40
 GC_FLAG_NO_BLOCK_BOUND = 0x80
+GC_FLAG_TILE_BARRIERS = 0x100
+GC_FLAG_DEBUG_PHASES = 0x200
+GC_FLAG_NO_SUP_SMEM = 0x400
 
 _STATUS = {0: "GC_OK", 1: "GC_EINVAL", 2: "GC_ERANGE", 3: "GC_ENOSPC", 4: "GC_EUNSUPPORTED",
            5: "GC_ECUDA", 6: "GC_ENOMEM", 7: "GC_ENCCL", 8: "GC_EINTERNAL"}
@@ -36,7 +39,10 @@ class gc_options(ctypes.Structure):
     _fields_ = [("struct_size", ctypes.c_uint32), ("tile_min", ctypes.c_uint32),
                 ("tile_max", ctypes.c_uint32), ("window0", ctypes.c_uint32),
                 ("emulate_ranks", ctypes.c_uint32), ("flags", ctypes.c_uint32),
-                ("window_growth", ctypes.c_uint32)]
+                ("window_growth", ctypes.c_uint32), ("pipeline_depth", ctypes.c_uint32),
+                ("target_accepted", ctypes.c_uint32), ("items_per_warp", ctypes.c_uint32),
+                ("sub_max", ctypes.c_uint32), ("geo_head", ctypes.c_uint32), ("split_bits", ctypes.c_uint32),
+                ("partial_s", ctypes.c_uint32), ("grid_ctas", ctypes.c_uint32), ("plan_warps", ctypes.c_uint32)]
 
 
 GC_B_ORDERING = 4
@@ -55,7 +61,10 @@ class gc_stats(ctypes.Structure):
                 ("checks_exec", ctypes.c_uint64), ("survivors", ctypes.c_uint64),
                 ("conflicts", ctypes.c_uint64), ("resolve_checks", ctypes.c_uint64),
                 ("w_def", ctypes.c_double), ("launches", ctypes.c_uint64),
-                ("screen_launches", ctypes.c_uint64), ("screen_ms", ctypes.c_double)]
+                ("screen_launches", ctypes.c_uint64), ("screen_ms", ctypes.c_double),
+                ("bound_tests", ctypes.c_uint64), ("resolve_wait_ms", ctypes.c_double),
+                ("resolve_busy_ms", ctypes.c_double), ("pipeline_depth", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
 
     def to_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_ if name != "struct_size"}
@@ -230,6 +239,8 @@ def _problem(n, d, ordering="lex", basis=None, constant_weight=-1, self_orthogon
     p.n, p.d = n, d
     keep = None
     if basis is not None:
+        if len(basis) != n:
+            raise ValueError(f"a B-ordering basis needs exactly n = {n} vectors, got {len(basis)}")
         keep = (ctypes.c_uint64 * len(basis))(*[int(x) for x in basis])
         p.basis = ctypes.cast(keep, ctypes.POINTER(ctypes.c_uint64))
         p.ordering = GC_B_ORDERING

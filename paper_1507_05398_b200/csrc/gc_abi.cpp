@@ -32,6 +32,20 @@ int resolve_options(const gc_options *opt, Options *out) {
         if (opt->emulate_ranks) o.emulate_ranks = opt->emulate_ranks;
         o.flags = opt->flags;
         if (opt->window_growth) o.growth = opt->window_growth;
+        o.pipeline_depth = opt->pipeline_depth;
+        o.target_accepted = opt->target_accepted;
+        o.items_per_warp = opt->items_per_warp;
+        o.sub_max = opt->sub_max;
+        o.geo_head = opt->geo_head;
+        o.split_bits = opt->split_bits;
+        o.partial_s = opt->partial_s;
+        o.grid_ctas = opt->grid_ctas;
+        o.plan_warps = opt->plan_warps;
+    }
+    if (o.pipeline_depth > 16 || (o.sub_max && o.sub_max < 64) || (o.partial_s && o.partial_s < 32) ||
+        o.split_bits > 32) {
+        set_error("pipeline_depth must be <= 16, sub_max >= 64, partial_s >= 32, split_bits <= 32");
+        return GC_EINVAL;
     }
     if (o.growth > 12) {          // 0 = engine default
         set_error("window_growth must be in [1, 12]");
@@ -52,7 +66,8 @@ int resolve_options(const gc_options *opt, Options *out) {
     }
     if (o.flags & ~(uint32_t)(GC_FLAG_NO_EARLY_EXIT | GC_FLAG_SYNC_TILES | GC_FLAG_FORCE_SEQ_RESOLVE |
                               GC_FLAG_KERNEL_TIMING | GC_FLAG_LAUNCHED_TILES | GC_FLAG_POPC_ONLY |
-                              GC_FLAG_NO_WEIGHT_BOUND | GC_FLAG_NO_BLOCK_BOUND)) {
+                              GC_FLAG_NO_WEIGHT_BOUND | GC_FLAG_NO_BLOCK_BOUND | GC_FLAG_TILE_BARRIERS |
+                              GC_FLAG_DEBUG_PHASES | GC_FLAG_NO_SUP_SMEM)) {
         set_error("unknown bits in gc_options.flags");
         return GC_EINVAL;
     }
@@ -323,6 +338,7 @@ int gc_generate_device(uint32_t n, uint32_t d, gc_ordering ordering, const gc_op
     rc = resolve_options(opt, &a.opt);
     if (rc) return rc;
     if (!d_codebook || !d_count || capacity == 0) { set_error("d_codebook/d_count NULL or capacity 0"); return GC_EINVAL; }
+    if ((uintptr_t)d_codebook & 15u) { set_error("d_codebook must be 16-byte aligned"); return GC_EINVAL; }
     if (stats && stats->struct_size != 0 && stats->struct_size < sizeof(gc_stats)) {
         set_error("gc_stats.struct_size too small");
         return GC_EINVAL;
@@ -345,6 +361,7 @@ int gc_construct_device(const gc_problem *problem, const gc_options *opt, uint32
     rc = resolve_options(opt, &a.opt);
     if (rc) return rc;
     if (!d_codebook || !d_count || capacity == 0) { set_error("d_codebook/d_count NULL or capacity 0"); return GC_EINVAL; }
+    if ((uintptr_t)d_codebook & 15u) { set_error("d_codebook must be 16-byte aligned"); return GC_EINVAL; }
     if (stats && stats->struct_size != 0 && stats->struct_size < sizeof(gc_stats)) {
         set_error("gc_stats.struct_size too small");
         return GC_EINVAL;
@@ -428,6 +445,7 @@ int gc_generate_rank(uint32_t n, uint32_t d, gc_ordering ordering, const gc_opti
     if (rc) return rc;
     if (comm && comm->world > 1 && a.opt.emulate_ranks != 1) { set_error("emulate_ranks needs a single rank"); return GC_EINVAL; }
     if (!d_codebook || !d_count || capacity == 0) { set_error("d_codebook/d_count NULL or capacity 0"); return GC_EINVAL; }
+    if ((uintptr_t)d_codebook & 15u) { set_error("d_codebook must be 16-byte aligned"); return GC_EINVAL; }
     if (stats && stats->struct_size != 0 && stats->struct_size < sizeof(gc_stats)) {
         set_error("gc_stats.struct_size too small");
         return GC_EINVAL;

@@ -418,7 +418,9 @@ k_commit(const uint2 *__restrict__ surv, const uint2 *__restrict__ edges, uint8_
     }
 }
 
-__global__ void k_finish(const DevCounters *ctr, unsigned long long *d_count) { *d_count = ctr->M; }
+__global__ void k_finish(const DevCounters *ctr, unsigned long long *d_count, unsigned long long capacity) {
+    *d_count = ctr->error ? capacity + 1 : ctr->M;     // above capacity: incomplete code (gc.h)
+}
 
 __global__ void k_unrank(const OrderTables *__restrict__ tab, int ord, int n, unsigned long long first,
                          unsigned long long count, uint32_t *__restrict__ out) {
@@ -529,10 +531,16 @@ int engine_run(const RunArgs &a) {
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
         return rc;
     }
-    if (a.extended() && !persistent_supported(a)) {
+    if (a.extended() && !pipeline_supported(a) && !persistent_supported(a)) {
         set_error("B-ordering / self-orthogonal / constant-weight problems run on the single-GPU persistent "
                   "engine only (no emulate_ranks, launched tiles, no-early-exit or sequential-resolve flags)");
         return GC_EUNSUPPORTED;
+    }
+    if (pipeline_supported(a)) {
+        int rc = pipeline_run(a);
+        if (a.stats) a.stats->wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+        return rc;
     }
     if (persistent_supported(a)) {
         int rc = persistent_run(a);
@@ -649,7 +657,7 @@ int engine_run(const RunArgs &a) {
         ++tile;
         if (o.flags & GC_FLAG_SYNC_TILES) CK(cudaStreamSynchronize(st));
     }
-    k_finish<<<1, 1, 0, st>>>(cx->ctr, (unsigned long long *)a.d_count);
+    k_finish<<<1, 1, 0, st>>>(cx->ctr, (unsigned long long *)a.d_count, a.capacity);
     ++launches;
     CK(cudaEventRecord(cx->ev1, st));
     CK(cudaGetLastError());
@@ -681,7 +689,7 @@ int engine_run(const RunArgs &a) {
             s->screen_ms += t;
         }
         s->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
-        if (getenv("GC_DEBUG_PHASES")) {
+        if (o.flags & GC_FLAG_DEBUG_PHASES) {
             for (int p = 0; p < kMaxPhases; ++p)
                 if (h.phase_alive[p])
                     fprintf(stderr, "[gc] phase %2d: alive %.4g  checks %.4g  (%.1f%% of screen)\n", p,

@@ -23,7 +23,11 @@ struct Options {
     uint32_t emulate_ranks = 1;
     uint32_t flags = 0;
     uint32_t growth = 0;            // log2 window growth per level, 0 = engine default (launched
-                                    // engine 2; persistent engine: see p_setup)
+                                    // engine 2; persistent engines: see p_fill_args)
+    // persistent engines (0 = default; gc.h gc_options)
+    uint32_t pipeline_depth = 0, target_accepted = 0, items_per_warp = 0, sub_max = 0, geo_head = 0,
+             split_bits = 0, partial_s = 0, grid_ctas = 0, plan_warps = 0;
+    bool geo_head_set = false;
 };
 int resolve_options(const gc_options *opt, Options *out);   // GC_OK / GC_EINVAL
 
@@ -67,6 +71,8 @@ int engine_run(const RunArgs &a);
 int gc_problem_to_args(const gc_problem *p, RunArgs *a);   // gc_abi.cpp (validation, no CUDA)
 int analyze_device(const uint32_t *d_words, uint64_t M, int pairwise, int orth, void *stream,
                    gc_analysis *out);                        // gc_analysis.cu
+bool pipeline_supported(const RunArgs &a);     // gc_pipeline.cu (default single-GPU engine)
+int pipeline_run(const RunArgs &a);
 bool persistent_supported(const RunArgs &a);   // gc_persistent.cu
 int persistent_run(const RunArgs &a);
 bool persistent_partitioned_supported(const RunArgs &a);

@@ -109,9 +109,10 @@ def test_cfg2_extended_golay(gc, ordering):
     w, st = gpu_code(gc, 24, 8, ordering)
     ref = SURVEY[(24, 8, ordering)]
     assert len(w) == 4096 == ref["M"]
+    assert np.array_equal(w, O.greedy_ball(24, 8, ordering))      # element by element (O2)
     assert format(O.seq_digest(w), "016x") == ref["seq_digest"]
+    assert format(O.set_digest(w), "016x") == ref["set_digest"]
     if ordering == "lex":
-        assert np.array_equal(w, O.greedy_ball(24, 8, "lex"))
         assert O.weight_distribution(w) == {0: 1, 8: 759, 12: 2576, 16: 759, 24: 1}
 
 
@@ -126,23 +127,36 @@ def test_cfg3_d3_sweep(gc, ordering, n):
         assert format(O.seq_digest(w), "016x") == SURVEY[(n, 3, ordering)]["seq_digest"]
 
 
-@pytest.mark.slow
-@pytest.mark.parametrize("ordering", ["gray", "glex"])
-def test_cfg4_26_4(gc, ordering):
-    w, st = gpu_code(gc, 26, 4, ordering)
-    assert len(w) == 1 << 20
-    assert np.array_equal(w, O.greedy_ball(26, 4, ordering))
-    assert format(O.seq_digest(w), "016x") == SURVEY[(26, 4, ordering)]["seq_digest"]
-
-
-@pytest.mark.slow
-def test_cfg5_28_3_lex(gc):
-    w, st = gpu_code(gc, 28, 3, "lex")
-    assert len(w) == 1 << 23
-    assert np.array_equal(w, O.greedy_ball(28, 3, "lex"))
-    ref = SURVEY[(28, 3, "lex")]
+def _check_survey_row(w, n, d, ordering):
+    ref = SURVEY[(n, d, ordering)]
+    assert len(w) == ref["M"]
+    assert w[:len(ref["first8"])].tolist() == ref["first8"]
+    assert int(w[-1]) == ref["last"]
     assert format(O.set_digest(w), "016x") == ref["set_digest"]
     assert format(O.seq_digest(w), "016x") == ref["seq_digest"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("ordering", ORDERS)
+def test_cfg4_26_4(gc, ordering):
+    # BASELINE configs[3] names Gray and graded-lex; the north_star asks for all four orders
+    w, st = gpu_code(gc, 26, 4, ordering)
+    assert len(w) == 1 << 20
+    assert np.array_equal(w, O.greedy_ball(26, 4, ordering))      # element by element (O2)
+    _check_survey_row(w, 26, 4, ordering)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("ordering", ORDERS)
+def test_cfg5_28_3(gc, ordering):
+    # BASELINE configs[4] (lex) and the north_star's "all four orderings up to n=28"
+    w, st = gpu_code(gc, 28, 3, ordering)
+    assert len(w) == 1 << 23
+    assert np.array_equal(w, O.greedy_ball(28, 3, ordering))      # element by element (O2)
+    _check_survey_row(w, 28, 3, ordering)
+    if ordering == "lex":
+        ranks = w.astype(np.int64)                                  # lex: rank = value
+        assert st["w_def"] == O.w_def(28, ranks)
 
 
 @pytest.mark.parametrize("n,d,o", [(20, 5, "lex"), (20, 5, "glex"), (19, 7, "grlex"), (23, 7, "glex"),
@@ -190,6 +204,9 @@ SCHEDULES = [
     {"flags": 192, "window0": 256},     # neither bound
     {"window_growth": 4, "window0": 64},
     {"flags": 16, "window_growth": 3, "window0": 128},
+    {"flags": 0x100},                   # tile-barrier persistent engine
+    {"flags": 0x100, "tile_min": 32, "tile_max": 1024, "window0": 32},
+    {"flags": 0x100 | 128},
 ]
 
 
@@ -230,6 +247,12 @@ def test_enospc(gc):
     with pytest.raises(gc.GCError) as e:
         gc.gc_generate_device(10, 3, "lex", cb, cnt, stats=True)
     assert e.value.name == "GC_ENOSPC"
+    # without stats: the count reports more than the capacity (never a silently truncated code)
+    for flags in (0, TB):
+        cnt.zero_()
+        gc.gc_generate_device(10, 3, "lex", cb, cnt, options={"flags": flags})
+        torch.cuda.synchronize()
+        assert int(cnt.item()) > 5
 
 
 def test_rank_entry_world1(gc):
@@ -246,21 +269,41 @@ def test_rank_entry_world1(gc):
     assert np.array_equal(cb[:M].cpu().numpy().view(np.uint32), O.greedy_ball(n, d, o))
 
 
-# ------------------------------------------------ engine knobs (environment, read per call)
+# ------------------------------------------------ engine knobs (gc_options; none changes the code)
 
-ENV_KNOBS = [
-    {"GC_PARTIAL_S": "32"},                     # cut almost every tile after 32 survivors
-    {"GC_PARTIAL_S": "4096", "GC_TARGET_ACCEPTED": "2048"},   # big tiles, multi-chunk resolves
-    {"GC_GRID": "1"},                           # one CTA does every level and every resolve
-    {"GC_GRID": "3", "GC_ITEMS_PER_WARP": "8"},
-    {"GC_SUB_MAX": "64"},                       # many tiny deep-level items
+TB = 0x100      # GC_FLAG_TILE_BARRIERS: the round-1 tile-synchronous persistent kernel
+
+ENGINE_KNOBS = [
+    # pipelined engine (default)
+    {"pipeline_depth": 1},                      # no overlap: every tile sees the latest codebook
+    {"pipeline_depth": 2},
+    {"pipeline_depth": 16, "tile_min": 32, "tile_max": 256},   # deep, tiny tiles: long prior ranges
+    {"pipeline_depth": 8, "target_accepted": 4096},            # big tiles: multi-chunk resolves
+    {"grid_ctas": 2},                           # one resolving CTA, one screening CTA
+    {"grid_ctas": 3, "items_per_warp": 8},
+    {"sub_max": 64},                            # many tiny items
+    {"plan_warps": 16},                         # few items per level
+    {"geo_head": 64, "split_bits": 1},
+    {"flags": 0x400},                           # no shared-memory super-block mirror
+    # tile-barrier engine
+    {"flags": TB, "partial_s": 32},             # cut almost every tile after 32 survivors
+    {"flags": TB, "partial_s": 4096, "target_accepted": 2048},   # big tiles, multi-chunk resolves
+    {"flags": TB, "grid_ctas": 1},              # one CTA does every level and every resolve
+    {"flags": TB, "grid_ctas": 3, "items_per_warp": 8},
+    {"flags": TB, "sub_max": 64},
 ]
 
 
-@pytest.mark.parametrize("env", ENV_KNOBS, ids=lambda e: "-".join(f"{k}{v}" for k, v in e.items()))
+@pytest.mark.parametrize("knobs", ENGINE_KNOBS, ids=lambda e: "-".join(f"{k}{v}" for k, v in e.items()))
 @pytest.mark.parametrize("n,d,o", [(18, 3, "lex"), (17, 4, "gray"), (16, 3, "glex"), (15, 5, "grlex")])
-def test_engine_knobs_invariance(gc, env, n, d, o, monkeypatch):
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    w, st = gpu_code(gc, n, d, o)
-    assert np.array_equal(w, O.greedy_ball(n, d, o)), env
+def test_engine_knobs_invariance(gc, knobs, n, d, o):
+    w, st = gpu_code(gc, n, d, o, **knobs)
+    assert np.array_equal(w, O.greedy_ball(n, d, o)), knobs
+
+
+def test_pipeline_stats(gc):
+    w, st = gpu_code(gc, 20, 3, "lex")
+    assert st["pipeline_depth"] == 4 and st["launches"] == 1
+    assert st["resolve_busy_ms"] > 0 and st["bound_tests"] > 0 and st["checks_exec"] > 0
+    w2, st2 = gpu_code(gc, 20, 3, "lex", flags=TB)
+    assert np.array_equal(w, w2) and st2["pipeline_depth"] == 0 and st2["bound_tests"] > 0

@@ -167,3 +167,35 @@ def test_no_constraint_reduces_to_base_greedy():
     for o in ("lex", "gray", "glex", "grlex"):
         for n, d in ((10, 3), (12, 4), (11, 5)):
             assert np.array_equal(O.greedy_ball_ex(n, d, o), O.greedy_ball(n, d, o))
+
+
+# ------------------------------------------- is_self_orthogonal: negative pins
+# a self-orthogonal code has every codeword "orthogonal to themselves and
+# to each other" (AND-parity even).  These fail a checker that returns 1 unconditionally,
+# skips the diagonal (a word against itself) or skips the off-diagonal pairs.
+
+def test_is_self_orthogonal_negative_golay23():
+    # the (23,7) lexicode is the [23,12,7] Golay code: odd weights 7, 11, ...
+    w = O.greedy_ball(23, 7, "lex")
+    assert len(w) == 4096
+    assert not O.is_self_orthogonal(w[:64])     # contains words of odd weight 7
+
+
+def test_is_self_orthogonal_negative_pair():
+    # 3 = 011, 5 = 101: both of even weight (each orthogonal to itself), 3 & 5 = 001 odd
+    assert O.orthogonal(3, 3) and O.orthogonal(5, 5)
+    assert not O.orthogonal(3, 5)
+    assert not O.is_self_orthogonal([3, 5])
+    assert not O.is_self_orthogonal([0, 3, 5])
+
+
+def test_is_self_orthogonal_negative_single_odd_word():
+    # a word of odd weight is not orthogonal to itself (the diagonal): 7 = 111
+    assert not O.is_self_orthogonal([7])
+    assert not O.is_self_orthogonal([0, 7])
+
+
+def test_is_self_orthogonal_positive_small():
+    assert O.is_self_orthogonal([])
+    assert O.is_self_orthogonal([0])
+    assert O.is_self_orthogonal([0, 3, 12, 15])     # [4,2] repetition pairs: 0011, 1100, 1111
