@@ -29,7 +29,7 @@ $(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o $(SRC)/gc_persistent.o $(SRC)/gc_pipe
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl -lpthread
 
 $(ORACLE): oracle/greedy_oracle.c
-	gcc -O2 -mpopcnt -Wall -shared -fPIC -o $@ $<
+	gcc -O2 -mpopcnt -Wall -pthread -shared -fPIC -o $@ $<
 
 clean:
 	rm -f $(SRC)/*.o $(LIB) $(ORACLE) $(SRC)/*.log

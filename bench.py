@@ -32,48 +32,11 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+from workloads import parse_workload, seq_digest, set_digest  # noqa: E402  (inputs + fingerprints only)
 
 # measured check rates (checks/clk/SM), profiles/r01_popc_peak.txt: the arithmetic the
 # kernel uses for each d (d <= 4: half of the checks in the ALU bit-clearing form)
 CHECK_PEAK_PER_CLK_SM = {"popc": 15.49, 2: 23.62, 3: 19.18, 4: 16.66}
-
-
-def parse_workload(s: str):
-    """n,d,ordering[,so][,cw=W][,basis=gray|std|seed:S] -> (n, d, ordering, extras)."""
-    parts = s.split(",")
-    n, d, o = int(parts[0]), int(parts[1]), parts[2]
-    ex = {}
-    for p in parts[3:]:
-        if p == "so":
-            ex["self_orthogonal"] = True
-        elif p.startswith("cw="):
-            ex["constant_weight"] = int(p[3:])
-        elif p.startswith("basis="):
-            kind = p[6:]
-            if kind == "gray":
-                ex["basis"] = [1] + [3 << (j - 1) for j in range(1, n)]
-            elif kind == "std":
-                ex["basis"] = [1 << j for j in range(n)]
-            elif kind.startswith("seed:"):
-                import random
-                rng = random.Random(int(kind[5:]))
-                while True:   # random invertible basis (seeded)
-                    b = [rng.randrange(1, 1 << n) for _ in range(n)]
-                    red = {}
-                    for x in b:
-                        while x:
-                            h = x.bit_length() - 1
-                            if h in red:
-                                x ^= red[h]
-                            else:
-                                red[h] = x
-                                break
-                    if len(red) == n:
-                        ex["basis"] = b
-                        break
-        else:
-            raise ValueError(f"unknown workload option {p}")
-    return n, d, o, ex
 
 
 def measured_peaks():
@@ -151,78 +114,125 @@ def load_traffic():
 
 # ------------------------------------------------------------------ CPU oracle
 
-def oracle_sample(n, d, ordering, budget_s=20.0, start_log2=16):
-    """The oracle (O1, plain serial greedy, Fig. 2(a)) as it stands, on a
-    bounded PREFIX of the same workload's scan: the first 2^k ranks, k grown until the
-    budget is used.  Returns (W_def of the prefix / seconds, description)."""
+def host_cpu():
+    """(threads this process may use, CPU model) of the host the bench runs on."""
+    cores = len(os.sched_getaffinity(0))
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return cores, model
+
+
+def golden_row(workload: str):
+    """Expected output of a bench workload (tests/golden/bench_golden.json, written by
+    tools/gen_bench_golden.py from oracle O2 alone), or None."""
+    try:
+        rows = json.load(open(os.path.join(ROOT, "tests", "golden", "bench_golden.json")))["rows"]
+    except Exception:
+        return None
+    for r in rows:
+        if r["workload"] == workload:
+            return r
+    return None
+
+
+def o2_full(n, d, o, ex):
+    """The oracle's exact greedy (O2, ball marking, one thread) on the WHOLE workload."""
+    import oracle as O
+    t = time.perf_counter()
+    w = O.greedy_ball_ex(n, d, o, **ex) if ex else O.greedy_ball(n, d, o)
+    return time.perf_counter() - t, w
+
+
+def o1_prefix(n, d, o, threads, budget_s, start_log2=16):
+    """The oracle's plain greedy (O1: Fig. 2(a) with threads == 1, the Fig. 2(b) thread
+    sections otherwise) on a bounded PREFIX of the workload's scan: the first
+    2^k ranks, k grown while the budget allows.  Returns (W_def of the prefix / s, text)."""
     import numpy as np
     import oracle as O
-    best = None
     k = min(start_log2, n)
-    spent = 0.0
+    spent, best = 0.0, None
+    full = O.order_table(o, n) if o not in ("lex", "gray") else None
     while True:
         nranks = 1 << k
-        if ordering in ("lex", "gray"):
-            # the first 2^k ranks of the n-bit lex / reflected Gray order are the k-bit order
-            table = O.order_table(ordering, k)
-        else:
-            table = O.order_table(ordering, n)[:nranks].copy()
+        # the first 2^k ranks of the n-bit lex / reflected Gray order are the k-bit order
+        table = O.order_table(o, k) if full is None else full[:nranks].copy()
         t = time.perf_counter()
-        w = O.greedy_plain(n, d, ordering, nranks=nranks, table=table)
+        if threads == 1:
+            w = O.greedy_plain(n, d, o, nranks=nranks, table=table)
+        else:
+            w = O.greedy_plain_mt(n, d, o, threads=threads, nranks=nranks, table=table)
         dt = time.perf_counter() - t
         spent += dt
-        # ranks of accepted words in the prefix: position in the table
-        pos = np.searchsorted(np.sort(table), w)
         inv = np.argsort(table)
-        ranks = inv[pos]
+        ranks = inv[np.searchsorted(np.sort(table), w)]
         wdef = int((nranks - 1 - ranks.astype(np.int64)).sum())
-        best = (wdef / dt, f"O1 on ranks [0, 2^{k}) of ({n},{d},{ordering}): M={len(w)}, "
-                           f"W_def={wdef:.4g} checks in {dt:.2f} s, 1 thread")
+        best = (wdef / dt, f"O1{'' if threads == 1 else '_mt'} on ranks [0, 2^{k}) of ({n},{d},{o}): M={len(w)}, "
+                           f"W_def={wdef:.4g} in {dt:.2f} s, {threads} thread(s)")
         if spent + 4 * dt > budget_s or k >= n:
             return best
         k += 1
 
 
+def cpu_baseline(n, d, o, ex, w_def, budget_s):
+    """The oracle timed on this host: O2 on the whole workload (value; the same config as the
+    GPU line), plus O1 single-threaded and O1 over all host threads on a bounded prefix."""
+    cores, model = host_cpu()
+    dt, w = o2_full(n, d, o, ex)
+    out = {"value": (w_def / dt) if w_def else None, "unit": "checks/s", "cores": 1, "kind": "oracle",
+           "sample": f"O2 (oracle/greedy_oracle.c or_greedy_ball: exact greedy by Hamming-ball marking) on the "
+                     f"whole workload ({n},{d},{o}), 1 thread: {dt:.2f} s per construction, M={len(w)}",
+           "seconds_per_construction": dt, "host_threads": cores, "cpu_model": model}
+    if not ex:
+        v1, s1 = o1_prefix(n, d, o, 1, budget_s / 2)
+        vm, sm = o1_prefix(n, d, o, cores, budget_s / 2)
+        out["o1_1thread"] = {"value": v1, "unit": "checks/s", "cores": 1, "sample": s1}
+        out["o1_threads"] = {"value": vm, "unit": "checks/s", "cores": cores, "sample": sm}
+    return out
+
+
 def run_reference(args):
+    """The reference arm: the oracle as it stands (O2, exact, one host thread) on the SAME
+    workload as the B200 arm, one whole construction per step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     n, d, o, ex = parse_workload(args.workload)
-    import numpy as np
-    import oracle as O
-    if ex:
-        print(json.dumps({"impl": "reference", "unavailable": "the reference arm times the base greedy only"}))
-        return 0
-    k = min(args.ref_log2, n)
-    nranks = 1 << k
-    table = O.order_table(o, k) if o in ("lex", "gray") else O.order_table(o, n)[:nranks].copy()
-    inv = np.argsort(table)
-    srt = np.sort(table)
-
-    def step():
-        t = time.perf_counter()
-        w = O.greedy_plain(n, d, o, nranks=nranks, table=table)
-        dt = time.perf_counter() - t
-        ranks = inv[np.searchsorted(srt, w)]
-        return dt, int((nranks - 1 - ranks.astype(np.int64)).sum())
-
+    g = golden_row(args.workload)
+    w_def = g.get("w_def") if g else None
     for _ in range(args.warmup):
-        step()
-    tot, wdef = 0.0, 0
+        o2_full(n, d, o, ex)
+    tot = 0.0
     for _ in range(args.steps):
-        dt, wd = step()
+        dt, w = o2_full(n, d, o, ex)
         tot += dt
-        wdef += wd
-    val = wdef / tot
-    sample = f"O1 (oracle/, plain serial greedy) on ranks [0, 2^{k}) of ({n},{d},{o}) per step, 1 thread"
+    ms = 1e3 * tot / args.steps
+    if w_def is None and not ex:
+        import oracle as O
+        import numpy as np
+        table = O.order_table(o, n)
+        inv = np.empty(1 << n, dtype=np.uint32)
+        inv[table] = np.arange(1 << n, dtype=np.uint32)
+        w_def = int(((1 << n) - 1 - inv[w].astype(np.int64)).sum())
+    val = (w_def / (ms * 1e-3)) if w_def else 1e3 / ms
+    unit = "checks/s" if w_def else "constructions/s"
+    cores, model = host_cpu()
+    sample = (f"O2 (oracle/, exact greedy by Hamming-ball marking) on the whole workload ({n},{d},{o}) per step, "
+              f"1 thread of {cores} ({model})")
     line = {
         "impl": "reference", "metric": "candidate-codeword distance checks/sec (definitional W_def)",
-        "value": val, "unit": "checks/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "strong",
+        "value": val, "unit": unit, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (the whole space F_2^n, no dataset)",
-        "config": {"workload": args.workload, "sample": sample},
-        "cpu_baseline": {"value": val, "unit": "checks/s", "cores": 1, "kind": "oracle", "sample": sample},
-        "e2e": {"value": val, "unit": "checks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": args.workload, "M": len(w), "w_def": w_def, "sample": sample},
+        "cpu_baseline": {"value": val, "unit": unit, "cores": 1, "kind": "oracle", "sample": sample,
+                         "host_threads": cores, "cpu_model": model},
+        "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -289,6 +299,22 @@ def run_b200(args):
     ms_per_step = max_ms / args.steps
     M = int(count.item())
     w_def = stats[-1]["w_def"]
+    # parity gate (outside the timed region): the constructed code against the oracle's
+    # (tests/golden/bench_golden.json, O2); a mismatch is not reported as a number
+    parity = "unchecked (no golden row for this workload)"
+    g = golden_row(args.workload)
+    if g is not None and rank == 0:
+        words = codebook[:M].cpu().numpy().view("uint32")
+        got = {"M": M, "seq_digest": format(seq_digest(words), "016x"), "set_digest": format(set_digest(words), "016x")}
+        want = {k: g[k] for k in got}
+        if not ex and "w_def" in g:
+            got["w_def"], want["w_def"] = int(w_def), g["w_def"]
+        if got != want:
+            print(json.dumps({"error": "parity gate: output differs from the oracle", "workload": args.workload,
+                              "got": got, "want": want}), flush=True)
+            return 3
+        parity = "O2-equal (M, sequence and set digests" + (", W_def" if "w_def" in got else "") + \
+                 " vs tests/golden/bench_golden.json)"
     value = w_def / (ms_per_step * 1e-3)
     if ex:
         # filtered problems have no definitional count over all ranks: report executed checks/s
@@ -395,9 +421,9 @@ def run_b200(args):
         }
         if ex:
             line["metric"] = "executed candidate-codeword checks/sec (W_exec; constrained problem)"
-        if world == 1 and not args.no_cpu_baseline and not ex:
-            v, desc = oracle_sample(n, d, o, budget_s=args.cpu_budget)
-            line["cpu_baseline"] = {"value": v, "unit": "checks/s", "cores": 1, "kind": "oracle", "sample": desc}
+        line["parity"] = parity
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(n, d, o, ex, w_def if not ex else None, args.cpu_budget)
         print(json.dumps(line), flush=True)
     comm.close()
     if world > 1:
@@ -414,7 +440,6 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--ref-log2", type=int, default=19, help="reference arm: ranks per step = 2^k")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -108,8 +108,7 @@ typedef struct gc_options {
 #define GC_FLAG_SYNC_TILES     0x2u  /* host waits after every tile (debugging)                         */
 #define GC_FLAG_FORCE_SEQ_RESOLVE 0x4u /* in-tile resolve by the sequential fallback (testing)           */
 #define GC_FLAG_LAUNCHED_TILES 0x10u /* host-launched tile kernels instead of the persistent
-                                        device-resident construction kernel (the multi-GPU and
-                                        emulate_ranks paths always use them)                      */
+                                        device-resident construction kernel (testing / comparison) */
 #define GC_FLAG_POPC_ONLY      0x20u /* every check by XOR+POPC (default for d <= 4: half of them
                                         by an ALU bit-clearing test of the same predicate)         */
 #define GC_FLAG_NO_WEIGHT_BOUND 0x40u /* graded orders: screen the whole codebook (default: stop at the
@@ -193,9 +192,9 @@ int gc_generate_device(uint32_t n, uint32_t d, gc_ordering ordering, const gc_op
  *     to itself (even weight) and to every accepted word (popcount(v & c) even);
  *   - constant-weight codes: only candidates of weight constant_weight.
  * The ordering still defines the scan; filtered candidates are never accepted.  Supported
- * by the single-GPU persistent engine (GC_EUNSUPPORTED with emulate_ranks > 1 or
- * GC_FLAG_LAUNCHED_TILES / NO_EARLY_EXIT / FORCE_SEQ_RESOLVE).  gc_stats.w_def is 0 for
- * filtered problems (its definition counts every rank). */
+ * by the persistent engines, single-GPU and partitioned (emulate_ranks > 1, world > 1);
+ * GC_EUNSUPPORTED with GC_FLAG_LAUNCHED_TILES / NO_EARLY_EXIT / FORCE_SEQ_RESOLVE.
+ * gc_stats.w_def is 0 for filtered problems (its definition counts every rank). */
 #define GC_B_ORDERING 4
 typedef struct gc_problem {
     uint32_t struct_size;        /* sizeof(gc_problem)                                        */

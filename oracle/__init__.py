@@ -40,7 +40,7 @@ def build(force: bool = False) -> str:
     """Compile greedy_oracle.c with plain gcc -O2 (no tuning flags)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         subprocess.check_call(
-            ["gcc", "-O2", "-mpopcnt", "-Wall", "-shared", "-fPIC", "-o", _SO, _SRC]
+            ["gcc", "-O2", "-mpopcnt", "-Wall", "-pthread", "-shared", "-fPIC", "-o", _SO, _SRC]
         )
     return _SO
 
@@ -56,6 +56,9 @@ def lib():
         L.or_greedy_plain.argtypes = [ctypes.c_int, ctypes.c_int, u32p, ctypes.c_uint64, u32p,
                                       ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
         L.or_greedy_plain.restype = ctypes.c_int64
+        L.or_greedy_plain_mt.argtypes = [ctypes.c_int, ctypes.c_int, u32p, ctypes.c_uint64, ctypes.c_int, u32p,
+                                         ctypes.c_uint64]
+        L.or_greedy_plain_mt.restype = ctypes.c_int64
         L.or_greedy_ball.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u32p, ctypes.c_uint64]
         L.or_greedy_ball.restype = ctypes.c_int64
         L.or_certify.argtypes = [ctypes.c_int, ctypes.c_int, u32p, u32p, ctypes.c_uint64,
@@ -138,6 +141,21 @@ def greedy_plain(n: int, d: int, ordering="lex", nranks: int | None = None, tabl
         raise RuntimeError(f"or_greedy_plain -> {M}")
     res = out[:M].copy()
     return (res, checks.value) if return_checks else res
+
+
+def greedy_plain_mt(n: int, d: int, ordering="lex", threads: int = 2, nranks: int | None = None,
+                    table=None) -> np.ndarray:
+    """O1 with the inner loop in `threads` sections (Fig. 2(b))."""
+    if table is None:
+        table = order_table(ordering, n)
+    N = 1 << n
+    nranks = N if nranks is None else nranks
+    cap = min(N, max(hamming_bound(n, d), 1)) if nranks == N else nranks
+    out = np.empty(max(cap, 1), dtype=np.uint32)
+    M = lib().or_greedy_plain_mt(n, d, _p(table), nranks, int(threads), _p(out), cap)
+    if M < 0:
+        raise RuntimeError(f"or_greedy_plain_mt -> {M}")
+    return out[:M].copy()
 
 
 def greedy_ball(n: int, d: int, ordering="lex") -> np.ndarray:

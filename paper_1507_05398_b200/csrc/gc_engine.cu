@@ -532,8 +532,8 @@ int engine_run(const RunArgs &a) {
         return rc;
     }
     if (a.extended() && !pipeline_supported(a) && !persistent_supported(a)) {
-        set_error("B-ordering / self-orthogonal / constant-weight problems run on the single-GPU persistent "
-                  "engine only (no emulate_ranks, launched tiles, no-early-exit or sequential-resolve flags)");
+        set_error("B-ordering / self-orthogonal / constant-weight problems run on the persistent engines "
+                  "only (not with launched tiles, no-early-exit or sequential-resolve flags)");
         return GC_EUNSUPPORTED;
     }
     if (pipeline_supported(a)) {

@@ -511,6 +511,7 @@ static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a) {
         o->launches = 1;
         o->screen_launches = 1;
         o->screen_ms = ms;
+        o->bound_tests = h.bound_tests;
         if (a.timing) {
             PState full;
             PCK(cudaMemcpy(&full, cx->st, sizeof(PState), cudaMemcpyDeviceToHost));
@@ -547,7 +548,7 @@ static int persistent_run_locked(const RunArgs &r, PContext *cx, PArgs &a) {
 // mask words (world > 1), then k_resolve_tile (one CTA; identical on every rank).  The
 // tile schedule is host-side and deterministic (every rank launches the same sequence).
 bool persistent_partitioned_supported(const RunArgs &a) {
-    return (a.world > 1 || a.opt.emulate_ranks > 1) && !a.extended() && (a.opt.tile_max == 0 || a.opt.tile_max <= kPMaxTile) &&
+    return (a.world > 1 || a.opt.emulate_ranks > 1) && (a.opt.tile_max == 0 || a.opt.tile_max <= kPMaxTile) &&
            !(a.opt.flags & (GC_FLAG_NO_EARLY_EXIT | GC_FLAG_FORCE_SEQ_RESOLVE | GC_FLAG_LAUNCHED_TILES));
 }
 
@@ -626,6 +627,7 @@ int persistent_run_partitioned(const RunArgs &r) {
         o->launches = launches;
         o->screen_launches = launches - tiles;
         o->screen_ms = ms;
+        o->bound_tests = h.bound_tests;
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }
     return GC_OK;

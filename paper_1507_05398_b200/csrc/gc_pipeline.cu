@@ -191,7 +191,10 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
                 ++s_issued;
             }
         }
-        unsigned long long t_wait = 0, t_busy = 0;
+        unsigned long long t_wait = 0, t_busy = 0, t_pub = 0;
+        PTimers tmr;
+        if (a.timing && threadIdx.x == 0) memset(&tmr, 0, sizeof tmr);
+        PTimers *timer = (a.timing && threadIdx.x == 0) ? &tmr : nullptr;
         for (unsigned long long i = 0;; ++i) {
             __syncthreads();
             if (i >= s_issued) break;
@@ -210,8 +213,9 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
             }
             __syncthreads();
             uint32_t *dead = a.qdead + (size_t)si * kQWords;
-            p_resolve(a, sm, s_t0[si], s_K[si], (int)s_L[si], pc, nullptr, 0, false, dead, s_Ms[si]);
+            p_resolve(a, sm, s_t0[si], s_K[si], (int)s_L[si], pc, timer, 0, false, dead, s_Ms[si]);
             if (threadIdx.x == 0) {
+                const unsigned long long tp = timer ? clock64() : 0;
                 // next descriptor: tile s_issued, screened against the codebook as of now
                 if (s_next < a.t_end) {
                     uint32_t Kn = p_next_tile(a, s_klast, pc.S_tile, pc.A_tile, s_t0[si] + s_K[si], pc.M, pc.S_last,
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
                 __threadfence();
                 q_st_release(&q->committed, i + 1);
                 t_busy += p_now();
+                if (timer) t_pub += clock64() - tp;
             }
         }
         if (threadIdx.x == 0) {
@@ -237,6 +242,10 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
             *a.d_count = __ldcg(&st->error) ? a.capacity + 1 : pc.M;   // above capacity: incomplete (gc.h)
             q->resolve_wait_ns = t_wait;
             q->resolve_busy_ns = t_busy;
+            if (timer) {
+                for (int k = 0; k < 8; ++k) st->t_r[k] = tmr.r[k];
+                st->t_sync = t_pub;
+            }
         }
     } else {
         // ------------------------------------------------------------------ screen
@@ -491,6 +500,20 @@ int pipeline_run(const RunArgs &r) {
         o->resolve_wait_ms = hq.resolve_wait_ns * 1e-6;
         o->resolve_busy_ms = hq.resolve_busy_ns * 1e-6;
         o->pipeline_depth = (uint32_t)a.depth;
+        if (a.timing) {
+            PState f;
+            QCK(cudaMemcpy(&f, cx->st, sizeof(PState), cudaMemcpyDeviceToHost));
+            const double T = (double)f.tiles, c = 1965.0;
+            fprintf(stderr, "[gc] pipeline: %llu tiles, depth %d, %.2f us/tile; resolver per tile: wait %.2f busy %.2f us\n",
+                    f.tiles, a.depth, ms * 1e3 / T, hq.resolve_wait_ns / T / 1e3, hq.resolve_busy_ns / T / 1e3);
+            fprintf(stderr, "[gc]   resolve: gather %.2f conflicts %.2f prior+status %.2f rounds %.2f sequential %.2f "
+                    "append %.2f clear+stats %.2f publish %.2f us (SM cycles at 1965 MHz)\n", f.t_r[0] / T / c,
+                    f.t_r[1] / T / c, f.t_r[5] / T / c, f.t_r[6] / T / c, f.t_r[2] / T / c, f.t_r[3] / T / c,
+                    f.t_r[4] / T / c, f.t_sync / T / c);
+            fprintf(stderr, "[gc]   per tile: survivors %.1f, accepted %.1f, resolve checks %.0f, levels %.2f; "
+                    "largest S %llu, %llu multi-chunk tiles, %.2f rounds, %.2f sequential\n", f.survivors / T, f.M / T,
+                    f.resolve_checks / T, f.levels / T, f.s_max, f.n_chunked, f.n_rounds / T, f.n_seq / T);
+        }
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }
     return GC_OK;

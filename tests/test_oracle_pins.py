@@ -287,3 +287,33 @@ def test_oracle_matches_survey_fingerprints(row):
     assert format(O.seq_digest(w), "016x") == row["seq_digest"]
     wd = O.w_def(n, rk)
     assert abs(wd - row["w_def"]) <= 1e-4 * row["w_def"]
+
+
+# ------------------------------- O1 with thread sections (Fig. 2(b))
+
+def test_plain_mt_example1():
+    # Example 1 with the inner loop split over 1..4 threads
+    e = PINS["example1"]
+    for T in (1, 2, 3, 4):
+        assert O.greedy_plain_mt(3, 2, "lex", threads=T).tolist() == e["output"]
+        for step, size in e["steps_sizes"].items():
+            assert len(O.greedy_plain_mt(3, 2, "lex", threads=T, nranks=int(step) - 1)) == size
+
+
+@pytest.mark.parametrize("ordering", ORDERS)
+@pytest.mark.parametrize("n", [4, 7, 9])
+def test_plain_mt_satisfies_greedy_characterisation(ordering, n):
+    t = O.order_table(ordering, n)
+    for d in range(1, n + 1):
+        for T in (2, 5):
+            w = O.greedy_plain_mt(n, d, ordering, threads=T, table=t)
+            assert brute_force_is_greedy_output(n, d, t, w), (n, d, T)
+
+
+@pytest.mark.parametrize("ordering", ORDERS)
+def test_plain_mt_hamming_sizes(ordering):
+    # d = 3 lexicode size = shortened Hamming code size 2^(n - ceil(log2(n+1))) (every ordering: P:231)
+    for n in (11, 14):
+        w = O.greedy_plain_mt(n, 3, ordering, threads=4)
+        assert len(w) == 1 << (n - math.ceil(math.log2(n + 1)))
+        assert np.array_equal(w, O.greedy_ball(n, 3, ordering))
