@@ -102,6 +102,13 @@ typedef struct gc_options {
                                 engine uses >= 2: one resolves, the others screen)                 */
     uint32_t plan_warps;     /* pipelined engine: warps a level's work items are planned for
                                 (default: screening warps / pipeline_depth)                        */
+    uint32_t prep_lead;      /* pipelined engine: a screening CTA prepares tile i (survivors, their
+                                check against the words committed since its screen, in-tile
+                                conflict lists) once tile i - prep_lead is being resolved; the
+                                resolver then checks only the newer words.  0 = default (2);
+                                GC_FLAG_NO_PREP: the resolver does everything                    */
+    uint32_t prep_ctas;      /* pipelined engine: CTAs that only prepare tiles (default 2; other
+                                screening CTAs also prepare when idle)                           */
 } gc_options;
 
 #define GC_FLAG_NO_EARLY_EXIT  0x1u  /* screen every candidate against the whole codebook, one phase     */
@@ -124,6 +131,10 @@ typedef struct gc_options {
                                         instead of the pipelined one (testing / comparison)          */
 #define GC_FLAG_DEBUG_PHASES   0x200u /* tile-barrier engine: per-phase timing and counters on stderr     */
 #define GC_FLAG_NO_SUP_SMEM    0x400u /* do not mirror the super-block summaries in shared memory          */
+#define GC_FLAG_NO_PREP        0x800u /* pipelined engine: no preparation of tiles by screening CTAs   */
+#define GC_FLAG_SIZE_ON_TRUE   0x1000u /* pipelined engine: size tiles on the survivors left after the
+                                        checks against the newest words (default: on the survivors of
+                                        the screen against the older codebook, which the resolve gets) */
 #define GC_FLAG_KERNEL_TIMING  0x8u  /* bracket every screen launch with CUDA events on the launching
                                         stream; fills gc_stats.screen_ms (benchmarking)               */
 
@@ -151,6 +162,7 @@ typedef struct gc_stats {
     double resolve_busy_ms;  /* pipelined engine: time it spent resolving and committing             */
     uint32_t pipeline_depth; /* pipelined engine: tiles in flight (0: another engine ran)             */
     uint32_t reserved;
+    uint64_t prep_used;      /* pipelined engine: tiles resolved from a screening CTA's preparation   */
 } gc_stats;
 
 /* ------------------------------------------------------------------ generate */
@@ -301,6 +313,20 @@ int gc_generate_rank(uint32_t n, uint32_t d, gc_ordering ordering, const gc_opti
  * never accepted) and rank r screens [r Kpad/world, (r+1) Kpad/world), a whole number of
  * 32-bit mask words, so the all-gather of the mask words rebuilds the tile's mask in rank
  * order.  GC_EINVAL for a bad world/rank or NULL outputs. */
+/* Multi-GPU pipelined engine (one process per GPU of one node, 2..8 ranks): every rank runs the
+ * persistent pipelined kernel on its own replica of the codebook and screens its partition of
+ * every tile (gc_tile_partition); the partition's survivor-mask words are stored straight into
+ * every peer's memory by the kernel (NVLink / NVSwitch peer stores, CUDA IPC mappings) with a
+ * per-tile flag, and every rank resolves the whole tile -- no host round trip and no collective
+ * in the data path.  Setup, once per communicator: every rank calls gc_peer_handles (the IPC
+ * handles of its exchange buffers on the current device, gc_peer_handle_bytes() bytes), the
+ * blobs are all-gathered in rank order (e.g. torch.distributed), and gc_comm_attach_peers opens
+ * them.  Without attached peers gc_generate_rank uses the tile-barrier engine with one NCCL
+ * all-gather per tile. */
+size_t gc_peer_handle_bytes(void);
+int gc_peer_handles(uint8_t *out, size_t out_bytes);
+int gc_comm_attach_peers(gc_comm *comm, const uint8_t *all_handles, size_t bytes_per_rank);
+
 int gc_tile_partition(uint32_t K, int world, int rank, uint32_t *part_lo, uint32_t *part_len,
                       uint32_t *Kpad);
 

@@ -20,6 +20,8 @@ from ._binding import (  # noqa: F401
     GC_FLAG_POPC_ONLY,
     GC_FLAG_SYNC_TILES,
     GC_FLAG_TILE_BARRIERS,
+    GC_FLAG_NO_PREP,
+    GC_FLAG_SIZE_ON_TRUE,
     GC_FLAG_DEBUG_PHASES,
     GC_FLAG_NO_SUP_SMEM,
     GC_B_ORDERING,
@@ -36,6 +38,7 @@ from ._binding import (  # noqa: F401
     gc_analyze,
     gc_analyze_device,
     gc_capacity_bound,
+    gc_comm_attach_peers,
     gc_comm_create,
     gc_comm_destroy,
     gc_construct,
@@ -47,6 +50,8 @@ from ._binding import (  # noqa: F401
     gc_last_error,
     gc_nccl_id_bytes,
     gc_nccl_unique_id,
+    gc_peer_handle_bytes,
+    gc_peer_handles,
     gc_rank_to_vector,
     gc_ranks_to_vectors,
     gc_ranks_to_vectors_device,

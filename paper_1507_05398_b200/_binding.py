@@ -28,6 +28,8 @@ GC_FLAG_POPC_ONLY = 0x20
 GC_FLAG_NO_WEIGHT_BOUND = 0x40
 GC_FLAG_NO_BLOCK_BOUND = 0x80
 GC_FLAG_TILE_BARRIERS = 0x100
+GC_FLAG_NO_PREP = 0x800
+GC_FLAG_SIZE_ON_TRUE = 0x1000
 GC_FLAG_DEBUG_PHASES = 0x200
 GC_FLAG_NO_SUP_SMEM = 0x400
 
@@ -42,7 +44,8 @@ class gc_options(ctypes.Structure):
                 ("window_growth", ctypes.c_uint32), ("pipeline_depth", ctypes.c_uint32),
                 ("target_accepted", ctypes.c_uint32), ("items_per_warp", ctypes.c_uint32),
                 ("sub_max", ctypes.c_uint32), ("geo_head", ctypes.c_uint32), ("split_bits", ctypes.c_uint32),
-                ("partial_s", ctypes.c_uint32), ("grid_ctas", ctypes.c_uint32), ("plan_warps", ctypes.c_uint32)]
+                ("partial_s", ctypes.c_uint32), ("grid_ctas", ctypes.c_uint32), ("plan_warps", ctypes.c_uint32),
+                ("prep_lead", ctypes.c_uint32), ("prep_ctas", ctypes.c_uint32)]
 
 
 GC_B_ORDERING = 4
@@ -64,7 +67,7 @@ class gc_stats(ctypes.Structure):
                 ("screen_launches", ctypes.c_uint64), ("screen_ms", ctypes.c_double),
                 ("bound_tests", ctypes.c_uint64), ("resolve_wait_ms", ctypes.c_double),
                 ("resolve_busy_ms", ctypes.c_double), ("pipeline_depth", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32)]
+                ("reserved", ctypes.c_uint32), ("prep_used", ctypes.c_uint64)]
 
     def to_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_ if name != "struct_size"}
@@ -120,6 +123,9 @@ _sig("gc_nccl_unique_id", ctypes.c_int, [_u8p, ctypes.c_size_t])
 _sig("gc_comm_create", ctypes.c_int, [_u8p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_void_p)])
 _sig("gc_comm_destroy", ctypes.c_int, [ctypes.c_void_p])
+_sig("gc_peer_handle_bytes", ctypes.c_size_t, [])
+_sig("gc_peer_handles", ctypes.c_int, [_u8p, ctypes.c_size_t])
+_sig("gc_comm_attach_peers", ctypes.c_int, [ctypes.c_void_p, _u8p, ctypes.c_size_t])
 _sig("gc_generate_rank", ctypes.c_int, [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int,
                                         ctypes.POINTER(gc_options), ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
@@ -382,6 +388,27 @@ def gc_comm_create(nccl_id: bytes | None, rank: int, world: int) -> GcComm:
 
 def gc_comm_destroy(comm: GcComm):
     comm.close()
+
+
+def gc_peer_handle_bytes() -> int:
+    return int(_lib.gc_peer_handle_bytes())
+
+
+def gc_peer_handles() -> bytes:
+    """CUDA IPC handles of this process's tile-exchange buffers on the current device."""
+    nb = gc_peer_handle_bytes()
+    buf = (ctypes.c_uint8 * nb)()
+    _check(_lib.gc_peer_handles(buf, nb), "gc_peer_handles")
+    return bytes(buf)
+
+
+def gc_comm_attach_peers(comm: GcComm, all_handles: bytes):
+    """Open every other rank's exchange buffers (all_handles: the ranks' gc_peer_handles, in rank order)."""
+    nb = gc_peer_handle_bytes()
+    if len(all_handles) != nb * comm.world:
+        raise ValueError(f"expected {comm.world} x {nb} bytes of handles, got {len(all_handles)}")
+    buf = (ctypes.c_uint8 * len(all_handles)).from_buffer_copy(all_handles)
+    _check(_lib.gc_comm_attach_peers(comm.handle, buf, nb), "gc_comm_attach_peers")
 
 
 def gc_generate_rank(n: int, d: int, ordering, comm: GcComm | None, codebook, count, stream=None,

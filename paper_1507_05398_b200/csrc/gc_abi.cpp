@@ -41,10 +41,13 @@ int resolve_options(const gc_options *opt, Options *out) {
         o.partial_s = opt->partial_s;
         o.grid_ctas = opt->grid_ctas;
         o.plan_warps = opt->plan_warps;
+        o.prep_lead = opt->prep_lead;
+        o.prep_ctas = opt->prep_ctas;
     }
     if (o.pipeline_depth > 16 || (o.sub_max && o.sub_max < 64) || (o.partial_s && o.partial_s < 32) ||
-        o.split_bits > 32) {
-        set_error("pipeline_depth must be <= 16, sub_max >= 64, partial_s >= 32, split_bits <= 32");
+        o.split_bits > 32 || o.prep_lead > 15 || o.prep_ctas > 64) {
+        set_error("pipeline_depth must be <= 16, sub_max >= 64, partial_s >= 32, split_bits <= 32, prep_lead <= 15, "
+                  "prep_ctas <= 64");
         return GC_EINVAL;
     }
     if (o.growth > 12) {          // 0 = engine default
@@ -67,7 +70,8 @@ int resolve_options(const gc_options *opt, Options *out) {
     if (o.flags & ~(uint32_t)(GC_FLAG_NO_EARLY_EXIT | GC_FLAG_SYNC_TILES | GC_FLAG_FORCE_SEQ_RESOLVE |
                               GC_FLAG_KERNEL_TIMING | GC_FLAG_LAUNCHED_TILES | GC_FLAG_POPC_ONLY |
                               GC_FLAG_NO_WEIGHT_BOUND | GC_FLAG_NO_BLOCK_BOUND | GC_FLAG_TILE_BARRIERS |
-                              GC_FLAG_DEBUG_PHASES | GC_FLAG_NO_SUP_SMEM)) {
+                              GC_FLAG_DEBUG_PHASES | GC_FLAG_NO_SUP_SMEM | GC_FLAG_NO_PREP |
+                              GC_FLAG_SIZE_ON_TRUE)) {
         set_error("unknown bits in gc_options.flags");
         return GC_EINVAL;
     }
@@ -407,6 +411,7 @@ int gc_tile_partition(uint32_t K, int world, int rank, uint32_t *part_lo, uint32
 struct gc_comm {
     int rank = 0, world = 1;
     void *nccl = nullptr;
+    PeerTable peers;          // the peers' exchange buffers (gc_comm_attach_peers)
 };
 
 int gc_comm_create(const uint8_t *nccl_id, size_t id_bytes, int rank, int world, gc_comm **out_comm) {
@@ -428,8 +433,25 @@ int gc_comm_create(const uint8_t *nccl_id, size_t id_bytes, int rank, int world,
     return GC_OK;
 }
 
+size_t gc_peer_handle_bytes(void) { return kPeerHandleBytes; }
+
+int gc_peer_handles(uint8_t *out, size_t out_bytes) {
+    clear_error();
+    if (!out || out_bytes < kPeerHandleBytes) { set_error("out must hold gc_peer_handle_bytes() bytes"); return GC_EINVAL; }
+    return pipeline_peer_handles(out);
+}
+
+int gc_comm_attach_peers(gc_comm *comm, const uint8_t *all, size_t bytes_per_rank) {
+    clear_error();
+    if (!comm || !all) { set_error("comm / handles NULL"); return GC_EINVAL; }
+    if (bytes_per_rank != kPeerHandleBytes) { set_error("bytes_per_rank must be gc_peer_handle_bytes()"); return GC_EINVAL; }
+    if (comm->world < 2 || comm->world > 8) { set_error("peers need 2..8 ranks (one node)"); return GC_EUNSUPPORTED; }
+    return pipeline_open_peers(&comm->peers, all, comm->world, comm->rank);
+}
+
 int gc_comm_destroy(gc_comm *comm) {
     if (!comm) return GC_OK;
+    pipeline_close_peers(&comm->peers);
     nccl_comm_destroy(comm->nccl);
     delete comm;
     return GC_OK;
@@ -453,7 +475,10 @@ int gc_generate_rank(uint32_t n, uint32_t d, gc_ordering ordering, const gc_opti
     a.n = n; a.d = d; a.ordering = ordering;
     a.d_codebook = d_codebook; a.capacity = capacity; a.d_count = d_count;
     a.stream = stream;
-    if (comm) { a.rank = comm->rank; a.world = comm->world; a.nccl_comm = comm->nccl; }
+    if (comm) {
+        a.rank = comm->rank; a.world = comm->world; a.nccl_comm = comm->nccl;
+        if (comm->peers.ready) a.peers = &comm->peers;
+    }
     gc_stats local{};
     a.stats = stats ? stats : &local;   // the multi-process call always synchronises
     return engine_run(a);

@@ -525,6 +525,14 @@ static int phases_for(unsigned long long M_ub, uint32_t W0, uint32_t growth) {
 
 int engine_run(const RunArgs &a) {
     auto wall0 = std::chrono::steady_clock::now();
+    // default: the pipelined engine (one GPU, emulated ranks, or one rank per GPU with attached
+    // peers); then the tile-barrier engines (GC_FLAG_TILE_BARRIERS, or ranks without peers)
+    if (pipeline_supported(a)) {
+        int rc = pipeline_run(a);
+        if (a.stats) a.stats->wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+        return rc;
+    }
     if (persistent_partitioned_supported(a)) {
         int rc = persistent_run_partitioned(a);
         if (a.stats) a.stats->wall_ms =
@@ -535,12 +543,6 @@ int engine_run(const RunArgs &a) {
         set_error("B-ordering / self-orthogonal / constant-weight problems run on the persistent engines "
                   "only (not with launched tiles, no-early-exit or sequential-resolve flags)");
         return GC_EUNSUPPORTED;
-    }
-    if (pipeline_supported(a)) {
-        int rc = pipeline_run(a);
-        if (a.stats) a.stats->wall_ms =
-            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
-        return rc;
     }
     if (persistent_supported(a)) {
         int rc = persistent_run(a);

@@ -26,7 +26,8 @@ struct Options {
                                     // engine 2; persistent engines: see p_fill_args)
     // persistent engines (0 = default; gc.h gc_options)
     uint32_t pipeline_depth = 0, target_accepted = 0, items_per_warp = 0, sub_max = 0, geo_head = 0,
-             split_bits = 0, partial_s = 0, grid_ctas = 0, plan_warps = 0;
+             split_bits = 0, partial_s = 0, grid_ctas = 0, plan_warps = 0, prep_lead = 0,
+             prep_ctas = 0;
     bool geo_head_set = false;
 };
 int resolve_options(const gc_options *opt, Options *out);   // GC_OK / GC_EINVAL
@@ -48,6 +49,18 @@ int nccl_comm_init(void **comm, int world, int rank, const uint8_t *id, size_t i
 int nccl_allgather_u32(const uint32_t *send, uint32_t *recv, size_t count_per_rank, void *comm, void *stream);
 void nccl_comm_destroy(void *comm);
 
+// ---- multi-GPU pipelined engine: the peers' tile-exchange buffers (CUDA IPC, gc_comm_attach_peers) ----
+struct PeerTable {
+    bool ready = false;
+    int world = 1, rank = 0;
+    uint32_t *qdead[8] = {nullptr};              // rank r's dead-mask ring (opened IPC mapping; own: null)
+    unsigned long long *qflags[8] = {nullptr};   // rank r's screen flags
+};
+constexpr size_t kPeerHandleBytes = 128;         // two cudaIpcMemHandle_t (qdead ring, flags)
+int pipeline_peer_handles(uint8_t *out);         // this process's handles (current device), kPeerHandleBytes
+int pipeline_open_peers(PeerTable *t, const uint8_t *all, int world, int rank);
+void pipeline_close_peers(PeerTable *t);
+
 // ---- engine (gc_engine.cu) ----
 struct RunArgs {
     uint32_t n, d;
@@ -55,6 +68,7 @@ struct RunArgs {
     Options opt;
     int rank = 0, world = 1;
     void *nccl_comm = nullptr;      // world > 1
+    const PeerTable *peers = nullptr;  // world > 1: attached peers (pipelined engine over NVLink)
     uint32_t *d_codebook = nullptr; // device, capacity words
     uint64_t capacity = 0;
     uint64_t *d_count = nullptr;    // device

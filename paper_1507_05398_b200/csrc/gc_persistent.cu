@@ -364,6 +364,9 @@ int persistent_run(const RunArgs &r) {
 // caller holds cx->mu
 static int p_setup(const RunArgs &r, PContext *cx, PArgs *pa) {
     cudaStream_t s = (cudaStream_t)r.stream;
+    // the context's buffers are reused by every call on this device: order this call after the
+    // previous one's kernels even when the callers use different streams
+    PCK(cudaStreamWaitEvent(s, cx->ev1, 0));
     if (cx->tabs_n != (int)r.n) {
         OrderTables t;
         build_order_tables((int)r.n, &t);

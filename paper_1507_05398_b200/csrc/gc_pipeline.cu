@@ -33,27 +33,53 @@
 
 namespace gc {
 
-constexpr int kQRing = 16;          // tile slots; the pipeline depth D <= kQRing
+constexpr int kQRing = kQRingMax;   // tile slots; the pipeline depth D <= kQRing (multi-rank: D <= 7)
+constexpr uint32_t kQChunk = 2048;  // survivors per resolve chunk (and per prepared tile)
 constexpr uint32_t kQWords = kPMaxTile / 32;
+constexpr unsigned long long kQM = (1ull << 40) - 1;   // QCtl::cm: committed tiles << 40 | M
+
+// QSlot::prep packs everything the resolver needs from a preparation into one word, so that
+// its CAS (or the poll that sees it finished) is the only round trip:
+//   tag (tile + 1, 12 bits) << 52 | state << 50 | (M_prep - M_s) (21 bits) << 29
+//     | S_prep (13 bits) << 16 | survivors of the screen (16 bits, saturated)
+// (M_prep - M_s counts the words committed since the tile's screen: < depth tiles x 2^16)
+constexpr unsigned kPrepOpen = 0, kPrepBusy = 1, kPrepDone = 2, kPrepResolver = 3;
+constexpr uint32_t kPrepTooMany = 0x1fff;           // S_prep: more survivors than one resolve chunk
+__host__ __device__ constexpr unsigned long long q_pw(unsigned long long i, unsigned st, unsigned long long dM = 0,
+                                                      uint32_t S = 0, uint32_t S_screen = 0) {
+    return (((i + 1) & 0xfffull) << 52) | ((unsigned long long)st << 50) | (dM << 29) |
+           ((unsigned long long)S << 16) | (S_screen > 0xffffu ? 0xffffu : S_screen);
+}
+__device__ __forceinline__ unsigned q_pw_state(unsigned long long w) { return (unsigned)(w >> 50) & 3u; }
+__device__ __forceinline__ unsigned long long q_pw_dM(unsigned long long w) { return (w >> 29) & ((1ull << 21) - 1); }
+__device__ __forceinline__ uint32_t q_pw_S(unsigned long long w) { return (uint32_t)(w >> 16) & 0x1fffu; }
+__device__ __forceinline__ uint32_t q_pw_Sscreen(unsigned long long w) { return (uint32_t)(w & 0xffffu); }
 
 // One tile in flight (global memory).  The descriptor fields are written by the resolver before
 // it releases `phase`; `items[l]` / `nlive[l]` for l >= 1 by the warp that finished level l - 1
-// before it releases `phase`.  Every reader acquires `phase` first and reads the rest from L2.
+// before it releases `phase`; the prepared survivors by the CTA that prepared the tile before it
+// releases `prep`.  Every reader acquires `phase` (or `prep`) first and reads the rest from L2.
 struct QSlot {
     unsigned long long phase;                   // (tile + 1) << 8 | level; level >= L: screened
+    unsigned long long prep;                    // q_pw(tile, state, M_prep, S_prep)
     unsigned long long t0, M_s, base;           // first rank; screened against codebook[base, M_s)
     uint32_t K, L;                              // candidates; levels
+    unsigned int inside;                        // CTAs between validating a level and their last claim
+    uint32_t pad;
     uint32_t items[kPMaxLevels];                // warp items of each level
     uint32_t nlive[kPMaxLevels];                // live candidates at the start of each level
     uint32_t done[kPMaxLevels];                 // items finished (arrival counter)
     unsigned long long claim[kPMaxLevels];      // ((tile + 1) mod 2^32) << 32 | items claimed
 };
 struct QCtl {
-    unsigned long long committed;               // tiles committed (release; the resolver only)
+    unsigned long long cm;                      // committed tiles << 40 | M after them (release; resolver)
     unsigned int finished;                      // every tile committed
     unsigned int pad;
     unsigned long long resolve_wait_ns;         // diagnostics: resolver time waiting for screens
     unsigned long long resolve_busy_ns;         //              and resolving
+    unsigned long long preps, prep_used;        // diagnostics: tiles prepared / resolved from a prep
+    unsigned long long prep_rchk;               // resolve checks done by preparations
+    unsigned long long busy_prep_ns;            // diagnostics: resolver busy time on prepared tiles
     QSlot slot[kQRing];
 };
 
@@ -67,31 +93,117 @@ __device__ __forceinline__ unsigned int q_ld_acquire32(const unsigned int *p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void q_st_release(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ __forceinline__ void q_st_release32(unsigned int *p, unsigned int v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// a strong store that, after a fence, completes a release pattern (PTX memory model)
+__device__ __forceinline__ void q_st_relaxed(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int q_atom_add_acqrel(unsigned int *p, unsigned int v) {
+    unsigned int old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long q_cas_acqrel(unsigned long long *p, unsigned long long cmp,
+                                                           unsigned long long val) {
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "l"(p), "l"(cmp), "l"(val)
+                 : "memory");
+    return old;
+}
 
-// Resolver thread 0: publish tile i (ranks [t0, t0 + K)) to be screened against
-// codebook[base, M_s).  Level 0 plans all K candidates; a tile with nothing to screen
-// (L == 0) is published as already screened.
-__device__ __forceinline__ void q_publish(const PArgs &a, QCtl *q, unsigned long long i, unsigned long long t0,
-                                          uint32_t K, unsigned long long M_s, unsigned long long base) {
+__device__ __forceinline__ unsigned long long q_ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void q_st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// This rank's share of a tile's screen: candidates [plo, plo + n0) of the K, whole 32-bit mask
+// words (the partition of gc_tile_partition: K padded to 32 x world, equal parts in rank order).
+__device__ __forceinline__ void q_part(const PArgs &a, uint32_t K, uint32_t &plo, uint32_t &n0) {
+    if (a.world <= 1) { plo = 0; n0 = K; return; }
+    const uint32_t qq = 32u * (uint32_t)a.world, kp = (K + qq - 1) / qq * qq, plen = kp / (uint32_t)a.world;
+    plo = (uint32_t)a.rank * plen;
+    n0 = plo < K ? min(plen, K - plo) : 0u;
+}
+
+// Every rank's partition of tile i (slot si) is in this rank's dead mask (multi-rank engine).
+__device__ __forceinline__ bool q_peers_in(const PArgs &a, int si, unsigned long long i) {
+    if (a.world <= 1) return true;
+    const unsigned long long *f = a.peer_flag[a.rank] + (size_t)si * kMaxRanks;
+    for (int g = 0; g < a.world; ++g)
+        if (q_ld_acquire_sys(f + g) != i + 1) return false;
+    return true;
+}
+
+// Multi-rank engine, one full warp: store this rank's partition words of tile i's dead mask into
+// every other rank's ring (peer memory over NVLink / NVSwitch, or another emulated rank's
+// buffer), then raise this rank's flag for the tile on every rank (after a system-scope fence).
+// data = false: the partition has nothing to send (empty, or no level ran).
+__device__ __forceinline__ void q_push(const PArgs &a, int si, unsigned long long i, uint32_t K, const uint32_t *dead,
+                                       bool data) {
+    if (a.world <= 1) return;
+    const int lane = threadIdx.x & 31;
+    if (data) {
+        uint32_t plo, n0;
+        q_part(a, K, plo, n0);
+        const uint32_t w_lo = plo / 32, w_hi = (plo + n0 + 31) / 32;
+        for (int g = 0; g < a.world; ++g) {
+            if (g == a.rank) continue;
+            uint32_t *dst = a.peer_qdead[g] + (size_t)si * kQWords;
+            for (uint32_t w = w_lo + lane; w < w_hi; w += 32) __stcg(dst + w, __ldcg(dead + w));
+        }
+    }
+    __threadfence_system();
+    __syncwarp();
+    if (lane < a.world) q_st_relaxed_sys(a.peer_flag[lane] + (size_t)si * kMaxRanks + a.rank, i + 1);
+    __syncwarp();
+}
+
+// Resolver thread 0, multi-rank engine: tile i was published with nothing for this rank to screen
+// (no level, or an empty partition): raise this rank's flag for it on every rank.
+__device__ __forceinline__ void q_flag_empty(const PArgs &a, int si, unsigned long long i) {
+    if (a.world <= 1) return;
+    __threadfence_system();
+    for (int g = 0; g < a.world; ++g) q_st_relaxed_sys(a.peer_flag[g] + (size_t)si * kMaxRanks + a.rank, i + 1);
+}
+
+// Resolver thread 0: make the slot of tile i reusable -- its previous tile is long committed, but
+// CTAs that validated one of its levels may still be about to claim items from it (a claim is an
+// add), so the counters are reset only once none is inside.  Done ahead of time (while waiting
+// for a screen) when the ring is deeper than the pipeline.
+__device__ __forceinline__ void q_reset(QCtl *q, unsigned long long i) {
+    QSlot &sl = q->slot[i % kQRing];
+    while (q_ld_acquire32(&sl.inside) != 0) __nanosleep(32);
+    const unsigned long long tag = (i + 1) & 0xffffffffull;
+    for (int l = 0; l < kPMaxLevels; ++l) { sl.claim[l] = tag << 32; sl.done[l] = 0; }
+}
+
+// Resolver thread 0: write the descriptor of tile i (ranks [t0, t0 + K)) to be screened against
+// codebook[base, M_s) into its (reset) slot.  Level 0 plans all K candidates; a tile with nothing
+// to screen (L == 0) is published as already screened.  Returns the phase word; the caller makes
+// everything visible with a fence and then stores it.
+__device__ __forceinline__ unsigned long long q_write(const PArgs &a, QCtl *q, unsigned long long i,
+                                                      unsigned long long t0, uint32_t K, unsigned long long M_s,
+                                                      unsigned long long base) {
     QSlot &sl = q->slot[i % kQRing];
     const int L = p_levels(M_s - base, a.W0, a.growth);
     sl.t0 = t0; sl.K = K; sl.M_s = M_s; sl.base = base; sl.L = (uint32_t)L;
-    const unsigned long long tag = (i + 1) & 0xffffffffull;
-    for (int l = 0; l < L; ++l) { sl.claim[l] = tag << 32; sl.done[l] = 0; sl.items[l] = 0; sl.nlive[l] = 0; }
-    if (L > 0) {
+    uint32_t plo, n0;
+    q_part(a, K, plo, n0);
+    if (L > 0 && n0 > 0) {
         long long hi, lo;
         p_level_window(a, M_s, base, L, 0, hi, lo);
-        sl.items[0] = (uint32_t)p_plan(a, K, hi - lo, a.plan_warps).items();
-        sl.nlive[0] = K;
+        sl.items[0] = (uint32_t)p_plan(a, n0, hi - lo, a.plan_warps).items();
+        sl.nlive[0] = n0;
     }
-    __threadfence();
-    q_st_release(&sl.phase, (i + 1) << 8);           // level 0 (>= L when L == 0: screened)
+    sl.prep = q_pw(i, kPrepOpen, 0, 0);
+    // the phase to open: level 0, or screened when this rank has nothing to screen
+    return ((i + 1) << 8) | (L > 0 && n0 > 0 ? 0u : (uint32_t)L);
 }
 
 // The warp that finished the last item of level l of tile i: merge the level's kills into the
@@ -102,9 +214,11 @@ __device__ __forceinline__ void q_finish_level(const PArgs &a, QSlot *sl, unsign
                                                uint32_t *dead, uint32_t *kill) {
     __threadfence();                                  // acquire side of the items' release
     const int lane = threadIdx.x & 31;
-    const uint32_t words = (K + 31) / 32;
+    uint32_t plo, n0;
+    q_part(a, K, plo, n0);
+    const uint32_t c_hi = plo + n0;
     uint32_t live = 0;
-    for (uint32_t w = lane; w < words; w += 32) {
+    for (uint32_t w = plo / 32 + lane; w < (c_hi + 31) / 32; w += 32) {
         const uint32_t k = __ldcg(kill + w);
         uint32_t dd = __ldcg(dead + w);
         if (k) {
@@ -113,7 +227,7 @@ __device__ __forceinline__ void q_finish_level(const PArgs &a, QSlot *sl, unsign
             __stcg(kill + w, 0u);
         }
         uint32_t lv = ~dd;
-        if (w * 32 + 32 > K) lv &= (1u << (K - w * 32)) - 1u;
+        if (w * 32 + 32 > c_hi) lv &= (1u << (c_hi - w * 32)) - 1u;
         live += __popc(lv);
     }
     live = __reduce_add_sync(0xffffffffu, live);
@@ -125,21 +239,39 @@ __device__ __forceinline__ void q_finish_level(const PArgs &a, QSlot *sl, unsign
         items = (uint32_t)p_plan(a, live, hi - lo, a.plan_warps).items();
     }
     if (items == 0) nl = L;                           // nothing left to screen
-    __threadfence();
     __syncwarp();
+    if (nl >= L) q_push(a, (int)(i % kQRing), i, K, dead, true);   // multi-rank: share the partition
     if (lane == 0) {
         if (nl < L) {
             sl->items[nl] = items;
             sl->nlive[nl] = live;
         }
         __threadfence();
-        q_st_release(&sl->phase, ((i + 1) << 8) | (unsigned)nl);
+        q_st_relaxed(&sl->phase, ((i + 1) << 8) | (unsigned)nl);
     }
     __syncwarp();
 }
 
-template <int kMinBlocks>
-__global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
+// the resolve scratch of a CTA in the dynamic shared memory (the level stages alias it)
+__device__ __forceinline__ PSmem q_smem(const PArgs &a, uint8_t *p_dyn, const uint32_t (*C)[33], const uint64_t *off,
+                                        const uint32_t *s_basis, uint32_t *s_ws, uint32_t *s_pre) {
+    PSmem sm;
+    const uint32_t ch = a.chunk;
+    sm.C = C; sm.off = off; sm.s_basis = s_basis; sm.s_ws = s_ws;
+    sm.s_val = reinterpret_cast<uint32_t *>(p_dyn);
+    sm.s_idx = reinterpret_cast<uint16_t *>(p_dyn + ch * 4);
+    sm.s_status = p_dyn + ch * 6;
+    sm.s_cnt = reinterpret_cast<uint32_t *>(p_dyn + ch * 8);
+    sm.s_adj = reinterpret_cast<uint16_t *>(p_dyn + ch * 12);
+    sm.chunk = ch;
+    sm.s_tmp = s_pre;                      // the level prefix area is free outside a level
+    sm.tmp_words = kPTmpMaxWords;
+    return sm;
+}
+
+// The whole construction as one persistent kernel body; `bid` is the CTA's index within its rank
+// (the kernel may hold several emulated ranks, each a group of CTAs).
+__device__ __forceinline__ void q_body(const PArgs &a, int bid) {
     const uint32_t kPChunk = a.chunk;
     __shared__ uint32_t C[33][33];
     __shared__ uint64_t off[34];
@@ -159,39 +291,35 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
     __syncthreads();
     const int lane = threadIdx.x & 31;
     unsigned long long my_checks = 0, my_tests = 0;
+    const PSmem sm = q_smem(a, p_dyn, C, off, s_basis, s_ws, s_pre);
 
-    if (blockIdx.x == 0) {
+    if (bid == 0) {
         // ------------------------------------------------------------------ resolver
-        PSmem sm;
-        sm.C = C; sm.off = off; sm.s_basis = s_basis; sm.s_ws = s_ws;
-        sm.s_val = reinterpret_cast<uint32_t *>(p_dyn);
-        sm.s_idx = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 4);
-        sm.s_status = p_dyn + kPChunk * 6;
-        sm.s_cnt = reinterpret_cast<uint32_t *>(p_dyn + kPChunk * 8);
-        sm.s_adj = reinterpret_cast<uint16_t *>(p_dyn + kPChunk * 12);
-        sm.chunk = kPChunk;
-        sm.s_tmp = s_pre;                      // this CTA never screens: the level prefix area is free
-        sm.tmp_words = kPTmpMaxWords;
         __shared__ PCount pc;
         __shared__ unsigned long long s_t0[kQRing], s_Ms[kQRing];
         __shared__ uint32_t s_K[kQRing], s_L[kQRing];
         __shared__ unsigned long long s_next, s_issued;
-        __shared__ uint32_t s_klast;
+        __shared__ int s_mode;
+        __shared__ PPrep s_pp;
+        const bool pre_reset = a.depth < kQRing;         // slot of tile i + D reset during tile i
         if (threadIdx.x == 0) {
             p_count_load(pc, st);
             s_next = a.t_begin;
             s_issued = 0;
-            s_klast = a.tile_min;
             // the first D tiles are screened against the empty codebook (nothing to screen)
             for (int i = 0; i < a.depth && s_next < a.t_end; ++i) {
                 const uint32_t K = (uint32_t)min((unsigned long long)a.tile_min, a.t_end - s_next);
                 s_t0[i] = s_next; s_K[i] = K; s_Ms[i] = 0; s_L[i] = 0;
-                q_publish(a, q, (unsigned long long)i, s_next, K, 0, 0);
+                q_reset(q, (unsigned long long)i);
+                const unsigned long long ph = q_write(a, q, (unsigned long long)i, s_next, K, 0, 0);
+                __threadfence();
+                q_st_relaxed(&q->slot[i].phase, ph);
+                q_flag_empty(a, i, (unsigned long long)i);        // nothing to screen (L == 0)
                 s_next += K;
                 ++s_issued;
             }
         }
-        unsigned long long t_wait = 0, t_busy = 0, t_pub = 0;
+        unsigned long long t_wait = 0, t_busy = 0, t_pub = 0, n_used = 0, t_bprep = 0, tb0 = 0;
         PTimers tmr;
         if (a.timing && threadIdx.x == 0) memset(&tmr, 0, sizeof tmr);
         PTimers *timer = (a.timing && threadIdx.x == 0) ? &tmr : nullptr;
@@ -202,66 +330,132 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
             QSlot *sl = &q->slot[si];
             if (threadIdx.x == 0) {
                 const unsigned long long tw = p_now();
-                for (;;) {
-                    const unsigned long long ph = q_ld_acquire(&sl->phase);
-                    if ((ph >> 8) == i + 1 && (uint32_t)(ph & 0xff) >= s_L[si]) break;
-                    __nanosleep(32);
+                if (pre_reset && s_next < a.t_end) q_reset(q, i + a.depth);
+                // Prepared by another CTA?  One CAS: it either hands over the finished preparation
+                // or takes the tile over (nobody started on it: this CTA does all of it).
+                int mode = 0;
+                bool need_phase = true;
+                if (a.prep_lead > 0) {
+                    const unsigned long long open = q_pw(i, kPrepOpen, 0, 0);
+                    unsigned long long w = q_cas_acqrel(&sl->prep, open, q_pw(i, kPrepResolver, 0, 0));
+                    if (w != open) {
+                        while (q_pw_state(w) != kPrepDone) { __nanosleep(32); w = q_ld_acquire(&sl->prep); }
+                        need_phase = false;               // prepared implies screened
+                        if (q_pw_S(w) != kPrepTooMany) {
+                            const uint8_t *buf = a.qprep + (size_t)si * p_prep_bytes(kPChunk);
+                            s_pp.S = q_pw_S(w);
+                            s_pp.S_screen = q_pw_Sscreen(w);
+                            s_pp.M_prep = s_Ms[si] + q_pw_dM(w);
+                            s_pp.val = reinterpret_cast<const uint32_t *>(buf);
+                            s_pp.cnt = reinterpret_cast<const uint32_t *>(buf + (size_t)kPChunk * 4);
+                            s_pp.idx = reinterpret_cast<const uint16_t *>(buf + (size_t)kPChunk * 8);
+                            s_pp.adj = reinterpret_cast<const uint16_t *>(buf + (size_t)kPChunk * 10);
+                            mode = 1;
+                            ++n_used;
+                        }
+                    }
                 }
+                if (need_phase) {
+                    for (;;) {
+                        const unsigned long long ph = q_ld_acquire(&sl->phase);
+                        if ((ph >> 8) == i + 1 && (uint32_t)(ph & 0xff) >= s_L[si] && q_peers_in(a, si, i)) break;
+                        __nanosleep(32);
+                    }
+                }
+                s_mode = mode;
                 const unsigned long long tb = p_now();
                 t_wait += tb - tw;
                 t_busy -= tb;
+                tb0 = tb;
             }
             __syncthreads();
             uint32_t *dead = a.qdead + (size_t)si * kQWords;
-            p_resolve(a, sm, s_t0[si], s_K[si], (int)s_L[si], pc, timer, 0, false, dead, s_Ms[si]);
+            p_resolve(a, sm, s_t0[si], s_K[si], (int)s_L[si], pc, timer, 0, false, dead, s_Ms[si],
+                      s_mode ? &s_pp : nullptr);
             if (threadIdx.x == 0) {
                 const unsigned long long tp = timer ? clock64() : 0;
-                // next descriptor: tile s_issued, screened against the codebook as of now
+                // next descriptor: tile s_issued, screened against the codebook as of now; its
+                // size follows the tile just resolved (p_resolve's pc.K_next)
+                unsigned long long ph = 0, *php = nullptr;
                 if (s_next < a.t_end) {
-                    uint32_t Kn = p_next_tile(a, s_klast, pc.S_tile, pc.A_tile, s_t0[si] + s_K[si], pc.M, pc.S_last,
-                                              pc.K_last ? pc.K_last : 1u);
-                    s_klast = Kn;
+                    uint32_t Kn = pc.K_next;
                     if ((unsigned long long)Kn > a.t_end - s_next) Kn = (uint32_t)(a.t_end - s_next);
                     const unsigned long long base = p_base(a, s_next, pc.M);
                     const int sj = (int)(s_issued % kQRing);
+                    if (!pre_reset) q_reset(q, s_issued);
                     s_t0[sj] = s_next; s_K[sj] = Kn; s_Ms[sj] = pc.M;
                     s_L[sj] = (uint32_t)p_levels(pc.M - base, a.W0, a.growth);
-                    q_publish(a, q, s_issued, s_next, Kn, pc.M, base);
+                    ph = q_write(a, q, s_issued, s_next, Kn, pc.M, base);
+                    php = &q->slot[sj].phase;
                     s_next += Kn;
                     ++s_issued;
                 }
+                // one fence releases the tile's appended words and summaries (the whole CTA's,
+                // ordered by the barrier at the end of p_resolve) and the new descriptor
                 __threadfence();
-                q_st_release(&q->committed, i + 1);
-                t_busy += p_now();
+                if (php) {
+                    q_st_relaxed(php, ph);
+                    if ((uint32_t)(ph & 0xff) >= s_L[(int)((s_issued - 1) % kQRing)])   // nothing to screen here
+                        q_flag_empty(a, (int)((s_issued - 1) % kQRing), s_issued - 1);
+                }
+                q_st_relaxed(&q->cm, ((i + 1) << 40) | pc.M);
+                const unsigned long long te = p_now();
+                t_busy += te;
+                if (s_mode) t_bprep += te - tb0;
                 if (timer) t_pub += clock64() - tp;
             }
         }
         if (threadIdx.x == 0) {
             q_st_release32(&q->finished, 1u);
+            pc.resolve_checks += __ldcg(&q->prep_rchk);   // every preparation was consumed (acquired)
             p_count_store(pc, st);
             *a.d_count = __ldcg(&st->error) ? a.capacity + 1 : pc.M;   // above capacity: incomplete (gc.h)
             q->resolve_wait_ns = t_wait;
             q->resolve_busy_ns = t_busy;
+            q->prep_used = n_used;
+            q->busy_prep_ns = t_bprep;
             if (timer) {
                 for (int k = 0; k < 8; ++k) st->t_r[k] = tmr.r[k];
                 st->t_sync = t_pub;
             }
         }
     } else {
-        // ------------------------------------------------------------------ screen
-        __shared__ unsigned long long s_tile, s_t0, s_Ms, s_base;
+        // ------------------------------------------------------------------ screen / prep
+        // CTAs 1 .. prep_ctas only prepare tiles for the resolver; the others screen, and prepare
+        // too when a tile is ready and they are between levels.
+        const bool prep_only = bid <= a.prep_ctas;
+        __shared__ unsigned long long s_tile, s_t0, s_Ms, s_base, s_Mc;
         __shared__ uint32_t s_K, s_L;
-        __shared__ int s_lvl;
-        unsigned long long hint = 0, supM = 0;
+        __shared__ int s_lvl;                 // >= 0: a level; -2: finished; -3: prepare s_tile
+        unsigned long long hint = 0, supM = 0, n_prep = 0;
         for (;;) {
             if (threadIdx.x == 0) {
                 int lvl = -1;
-                unsigned long long pick = 0;
+                unsigned long long pick = 0, Mc = 0;
                 unsigned int nap = 32;
                 for (;;) {
-                    const unsigned long long com = q_ld_acquire(&q->committed);
+                    const unsigned long long cmv = q_ld_acquire(&q->cm);
+                    const unsigned long long com = cmv >> 40;
+                    // 1. prepare a screened tile the resolver reaches soon (its critical path)
+                    for (unsigned long long j = com + 1; a.prep_lead > 0 && j <= com + (unsigned long long)a.prep_lead &&
+                                                         j < com + (unsigned long long)a.depth; ++j) {
+                        QSlot *sl = &q->slot[j % kQRing];
+                        const unsigned long long ph = q_ld_acquire(&sl->phase);
+                        if ((ph >> 8) != j + 1 || (uint32_t)(ph & 0xff) < __ldcg(&sl->L)) continue;
+                        if (!q_peers_in(a, (int)(j % kQRing), j)) continue;
+                        const unsigned long long open = q_pw(j, kPrepOpen, 0, 0);
+                        if (__ldcg(&sl->prep) != open) continue;
+                        if (atomicCAS(&sl->prep, open, q_pw(j, kPrepBusy, 0, 0)) == open) {
+                            pick = j;
+                            Mc = cmv & kQM;
+                            lvl = -3;
+                            break;
+                        }
+                    }
+                    if (lvl == -3) break;
+                    // 2. a level with items left
                     if (hint < com) hint = com;
-                    for (unsigned long long i = hint; i < com + (unsigned long long)a.depth; ++i) {
+                    for (unsigned long long i = hint; !prep_only && i < com + (unsigned long long)a.depth; ++i) {
                         QSlot *sl = &q->slot[i % kQRing];
                         const unsigned long long ph = q_ld_acquire(&sl->phase);
                         if ((ph >> 8) != i + 1) break;           // not published yet
@@ -272,22 +466,29 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
                         }
                         const unsigned long long c = __ldcg(&sl->claim[l]);
                         if ((c >> 32) == ((i + 1) & 0xffffffffull) && (uint32_t)c < __ldcg(&sl->items[l])) {
-                            pick = i;
-                            lvl = (int)l;
-                            break;
+                            // validate with the slot pinned: once `inside` is raised the slot is not
+                            // reset before this CTA's last claim
+                            q_atom_add_acqrel(&sl->inside, 1u);
+                            if (q_ld_acquire(&sl->phase) == ph) {
+                                pick = i;
+                                lvl = (int)l;
+                                break;
+                            }
+                            atomicSub(&sl->inside, 1u);
                         }
                     }
                     if (lvl >= 0) break;
                     if (q_ld_acquire32(&q->finished)) { lvl = -2; break; }
                     __nanosleep(nap);
-                    if (nap < 512) nap *= 2;
+                    if (nap < (prep_only ? 64u : 512u)) nap *= 2;
                 }
                 s_lvl = lvl;
-                if (lvl >= 0) {
+                if (lvl >= 0 || lvl == -3) {
                     QSlot *sl = &q->slot[pick % kQRing];
                     s_tile = pick;
                     s_t0 = __ldcg(&sl->t0); s_Ms = __ldcg(&sl->M_s); s_base = __ldcg(&sl->base);
                     s_K = __ldcg(&sl->K); s_L = __ldcg(&sl->L);
+                    s_Mc = Mc;
                 }
             }
             __syncthreads();
@@ -298,8 +499,25 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
             const int L = (int)s_L;
             const int si = (int)(i % kQRing);
             QSlot *sl = &q->slot[si];
-            const unsigned long long tag = (i + 1) & 0xffffffffull;
             uint32_t *dead = a.qdead + (size_t)si * kQWords, *kill = a.qkill + (size_t)si * kQWords;
+            if (l == -3) {
+                // ---- prepare tile i for the resolver
+                unsigned long long rchk = 0;
+                uint32_t S1 = 0;
+                const uint32_t S2 = p_prep(a, sm, t0, K, L, dead, M_s, s_Mc,
+                                           a.qprep + (size_t)si * p_prep_bytes(kPChunk),
+                                           a.qspill + (size_t)si * kPMaxTile, rchk, S1);
+                for (int o = 16; o > 0; o >>= 1) rchk += __shfl_down_sync(0xffffffffu, rchk, o);
+                if (lane == 0 && rchk) atomicAdd(&q->prep_rchk, rchk);
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    q_st_relaxed(&sl->prep, q_pw(i, kPrepDone, s_Mc - M_s, S2 == 0xffffffffu ? kPrepTooMany : S2, S1));
+                    ++n_prep;
+                }
+                continue;
+            }
+            const unsigned long long tag = (i + 1) & 0xffffffffull;
             if (a.nsup_smem && M_s > supM) {
                 // super-block summaries the commits since the last refresh changed (a summary that
                 // also covers words beyond M_s is still valid: it only widens)
@@ -310,15 +528,17 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
             }
             long long hi, lo;
             p_level_window(a, M_s, base, L, l, hi, lo);
-            uint32_t n_l = K;
-            if (l > 0) n_l = p_live_prefix(dead, 0, K, s_live, s_pre, s_ws);    // ends with a barrier
+            uint32_t plo, n0;
+            q_part(a, K, plo, n0);                            // this rank's candidates of the tile
+            uint32_t n_l = n0;
+            if (l > 0) n_l = p_live_prefix(dead, plo, plo + n0, s_live, s_pre, s_ws);    // ends with a barrier
             else __syncthreads();
             const PPlan pl = p_plan(a, n_l, hi - lo, a.plan_warps);
             PLevel lv;
             lv.l = l; lv.n_l = n_l; lv.B = pl.B; lv.nsub = pl.nsub;
             lv.hi = hi; lv.lo = lo; lv.sub = pl.sub; lv.t0 = t0; lv.head = pl.head; lv.J0 = pl.J0;
-            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = (K + 31) / 32; lv.basis = s_basis;
-            lv.stage = reinterpret_cast<uint32_t *>(p_dyn); lv.s_sup = s_sup; lv.c_lo = 0; lv.w_base = 0;
+            lv.s_pre = s_pre; lv.s_live = s_live; lv.words = (plo + n0 + 31) / 32 - plo / 32; lv.basis = s_basis;
+            lv.stage = reinterpret_cast<uint32_t *>(p_dyn); lv.s_sup = s_sup; lv.c_lo = plo; lv.w_base = plo;
             lv.kill = kill; lv.vals = a.qvals + (size_t)si * kPMaxTile;
             lv.win = nullptr; lv.wsum = nullptr; lv.win_lo = 0;
             if (p_window_in_smem(a, l, hi, lo))
@@ -338,7 +558,9 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
                 if (dn + 1 == (uint32_t)items) q_finish_level(a, sl, i, l, L, K, M_s, base, dead, kill);
             }
             __syncthreads();                                  // shared memory is reused by the next pick
+            if (threadIdx.x == 0) atomicSub(&sl->inside, 1u); // after this CTA's last claim on the slot
         }
+        if (threadIdx.x == 0 && n_prep) atomicAdd(&q->preps, n_prep);
     }
     for (int o = 16; o > 0; o >>= 1) {
         my_checks += __shfl_down_sync(0xffffffffu, my_checks, o);
@@ -348,18 +570,46 @@ __global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) {
     if (lane == 0 && my_tests) atomicAdd(&st->bound_tests, my_tests);
 }
 
+// One rank per launch (single GPU, or one process of the multi-GPU engine).
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline(PArgs a) { q_body(a, (int)blockIdx.x); }
+
+// Emulated ranks on one GPU (gc_options.emulate_ranks): gridDim.x / ngroups CTAs per rank, each
+// group with its own arguments (its replica of the codebook and of the pipeline state).
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kPThreads, kMinBlocks) k_pipeline_ranks(const PArgs *__restrict__ ga, int ngroups) {
+    __shared__ PArgs s_a;
+    const int per = (int)gridDim.x / ngroups, g = (int)blockIdx.x / per;
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(ga + g);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(&s_a);
+    for (int k = threadIdx.x; k < (int)(sizeof(PArgs) / 4); k += blockDim.x) dst[k] = __ldg(src + k);
+    __syncthreads();
+    q_body(s_a, (int)blockIdx.x - g * per);
+}
+
 // ------------------------------------------------------------------ host side
 
-struct QContext {
-    int device = -1, sms = 0;
-    uint2 *surv = nullptr;
+// One rank's device state: this process's rank, or an emulated one (gc_options.emulate_ranks).
+struct QRank {
+    uint2 *surv = nullptr, *qspill = nullptr;
     uint32_t *bsum = nullptr;
     size_t bsum_words = 0;
     PState *st = nullptr;
-    OrderTables *tabs = nullptr;
-    int tabs_n = -1;
     QCtl *q = nullptr;
     uint32_t *qdead = nullptr, *qkill = nullptr, *qvals = nullptr;
+    uint8_t *qprep = nullptr;
+    unsigned long long *qflags = nullptr;         // [kQRing][kMaxRanks]
+    uint32_t *codebook = nullptr;                 // emulated ranks > 0: their replica of the codebook
+    size_t cb_words = 0;
+    unsigned long long *count = nullptr;
+};
+
+struct QContext {
+    int device = -1, sms = 0;
+    OrderTables *tabs = nullptr;
+    int tabs_n = -1;
+    QRank rk[kMaxRanks];
+    PArgs *d_args = nullptr;                      // emulated ranks: their arguments
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::mutex mu;
 };
@@ -376,6 +626,21 @@ struct QContext {
 static std::mutex g_qmu;
 static QContext *g_qctx[64];
 
+static int q_rank_alloc(QRank &k) {
+    if (k.st) return GC_OK;
+    QCK(cudaMalloc(&k.surv, kPMaxTile * sizeof(uint2)));
+    QCK(cudaMalloc(&k.st, sizeof(PState)));
+    QCK(cudaMalloc(&k.q, sizeof(QCtl)));
+    QCK(cudaMalloc(&k.qdead, (size_t)kQRing * kQWords * 4));
+    QCK(cudaMalloc(&k.qkill, (size_t)kQRing * kQWords * 4));
+    QCK(cudaMalloc(&k.qvals, (size_t)kQRing * kPMaxTile * 4));
+    QCK(cudaMalloc(&k.qprep, (size_t)kQRing * p_prep_bytes(kQChunk)));
+    QCK(cudaMalloc(&k.qspill, (size_t)kQRing * kPMaxTile * sizeof(uint2)));
+    QCK(cudaMalloc(&k.qflags, (size_t)kQRing * kMaxRanks * sizeof(unsigned long long)));
+    QCK(cudaMalloc(&k.count, sizeof(unsigned long long)));
+    return GC_OK;
+}
+
 static int q_context(QContext **out) {
     int device;
     QCK(cudaGetDevice(&device));
@@ -386,25 +651,91 @@ static int q_context(QContext **out) {
         c = new QContext;
         c->device = device;
         QCK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
-        QCK(cudaMalloc(&c->surv, kPMaxTile * sizeof(uint2)));
-        QCK(cudaMalloc(&c->st, sizeof(PState)));
         QCK(cudaMalloc(&c->tabs, sizeof(OrderTables)));
-        QCK(cudaMalloc(&c->q, sizeof(QCtl)));
-        QCK(cudaMalloc(&c->qdead, (size_t)kQRing * kQWords * 4));
-        QCK(cudaMalloc(&c->qkill, (size_t)kQRing * kQWords * 4));
-        QCK(cudaMalloc(&c->qvals, (size_t)kQRing * kPMaxTile * 4));
+        QCK(cudaMalloc(&c->d_args, kMaxRanks * sizeof(PArgs)));
         QCK(cudaEventCreate(&c->ev0));
         QCK(cudaEventCreate(&c->ev1));
+        int rc = q_rank_alloc(c->rk[0]);
+        if (rc) return rc;
         g_qctx[device] = c;
     }
     *out = c;
     return GC_OK;
 }
 
+// ---- multi-GPU: the exchange buffers of rank 0 of this device's context, shared by CUDA IPC
+int pipeline_peer_handles(uint8_t *out) {
+    QContext *cx;
+    int rc = q_context(&cx);
+    if (rc) return rc;
+    cudaIpcMemHandle_t h[2];
+    QCK(cudaIpcGetMemHandle(&h[0], cx->rk[0].qdead));
+    QCK(cudaIpcGetMemHandle(&h[1], cx->rk[0].qflags));
+    static_assert(2 * sizeof(cudaIpcMemHandle_t) == kPeerHandleBytes, "handle blob size");
+    memcpy(out, h, sizeof h);
+    return GC_OK;
+}
+
+int pipeline_open_peers(PeerTable *t, const uint8_t *all, int world, int rank) {
+    if (world < 2 || world > kMaxRanks || rank < 0 || rank >= world) {
+        set_error("peers: world must be in [2, 8] and 0 <= rank < world");
+        return GC_EINVAL;
+    }
+    pipeline_close_peers(t);
+    for (int g = 0; g < world; ++g) {
+        if (g == rank) continue;
+        cudaIpcMemHandle_t h[2];
+        memcpy(h, all + (size_t)g * kPeerHandleBytes, sizeof h);
+        void *pd = nullptr, *pf = nullptr;
+        QCK(cudaIpcOpenMemHandle(&pd, h[0], cudaIpcMemLazyEnablePeerAccess));
+        QCK(cudaIpcOpenMemHandle(&pf, h[1], cudaIpcMemLazyEnablePeerAccess));
+        t->qdead[g] = static_cast<uint32_t *>(pd);
+        t->qflags[g] = static_cast<unsigned long long *>(pf);
+    }
+    t->world = world;
+    t->rank = rank;
+    t->ready = true;
+    return GC_OK;
+}
+
+void pipeline_close_peers(PeerTable *t) {
+    for (int g = 0; g < kMaxRanks; ++g) {
+        if (t->qdead[g]) cudaIpcCloseMemHandle(t->qdead[g]);
+        if (t->qflags[g]) cudaIpcCloseMemHandle(t->qflags[g]);
+        t->qdead[g] = nullptr;
+        t->qflags[g] = nullptr;
+    }
+    t->ready = false;
+}
+
 bool pipeline_supported(const RunArgs &a) {
-    return a.world == 1 && a.opt.emulate_ranks == 1 && a.opt.tile_max <= kPMaxTile &&
+    const bool ranks_ok = a.world == 1 ? (a.opt.emulate_ranks >= 1 && a.opt.emulate_ranks <= (uint32_t)kMaxRanks)
+                                       : (a.world <= kMaxRanks && a.opt.emulate_ranks == 1 && a.peers && a.peers->ready &&
+                                          a.peers->world == a.world && a.peers->rank == a.rank);
+    return ranks_ok && a.opt.tile_max <= kPMaxTile &&
            !(a.opt.flags & (GC_FLAG_NO_EARLY_EXIT | GC_FLAG_FORCE_SEQ_RESOLVE | GC_FLAG_LAUNCHED_TILES |
                             GC_FLAG_TILE_BARRIERS));
+}
+
+// per-call state of one rank: counters, pipeline, summaries (AND = all ones, OR = 0 before any
+// append, as in gc_persistent.cu)
+static int q_rank_reset(QRank &k, const RunArgs &r, cudaStream_t s, size_t nblk, size_t nsup) {
+    QCK(cudaMemsetAsync(k.st, 0, sizeof(PState), s));
+    QCK(cudaMemsetAsync(k.q, 0, sizeof(QCtl), s));
+    QCK(cudaMemsetAsync(k.qdead, 0, (size_t)kQRing * kQWords * 4, s));
+    QCK(cudaMemsetAsync(k.qkill, 0, (size_t)kQRing * kQWords * 4, s));
+    QCK(cudaMemsetAsync(k.qflags, 0, (size_t)kQRing * kMaxRanks * sizeof(unsigned long long), s));
+    const size_t need = 2 * (nblk + nsup);
+    if (k.bsum_words < need) {
+        if (k.bsum) QCK(cudaFree(k.bsum));
+        k.bsum = nullptr;
+        k.bsum_words = 0;
+        QCK(cudaMalloc(&k.bsum, need * 4));
+        k.bsum_words = need;
+    }
+    QCK(cudaMemsetAsync(k.bsum, 0, need * 4, s));
+    QCK(cudaMemset2DAsync(k.bsum, 8, 0xff, 4, nblk + nsup, s));
+    return GC_OK;
 }
 
 int pipeline_run(const RunArgs &r) {
@@ -413,42 +744,52 @@ int pipeline_run(const RunArgs &r) {
     if (rc) return rc;
     std::lock_guard<std::mutex> lock(cx->mu);       // setup, launch and read-back (gc.h)
     cudaStream_t s = (cudaStream_t)r.stream;
+    // the context's buffers are reused by every call on this device: order this call after the
+    // previous one's kernel even when the callers use different streams
+    QCK(cudaStreamWaitEvent(s, cx->ev1, 0));
     if (cx->tabs_n != (int)r.n) {
         OrderTables t;
         build_order_tables((int)r.n, &t);
         QCK(cudaMemcpy(cx->tabs, &t, sizeof t, cudaMemcpyHostToDevice));
         cx->tabs_n = (int)r.n;
     }
-    QCK(cudaMemsetAsync(cx->st, 0, sizeof(PState), s));
-    QCK(cudaMemsetAsync(cx->q, 0, sizeof(QCtl), s));
-    QCK(cudaMemsetAsync(cx->qdead, 0, (size_t)kQRing * kQWords * 4, s));
-    QCK(cudaMemsetAsync(cx->qkill, 0, (size_t)kQRing * kQWords * 4, s));
-    // block-bound summaries (AND = all ones, OR = 0 before any append), as in gc_persistent.cu
+    const int world = r.world > 1 ? r.world : (int)r.opt.emulate_ranks;   // ranks sharing each tile's screen
+    const int local = r.world > 1 ? 1 : world;                             // of which run in this launch
     const size_t nsup = (size_t)((r.capacity + 1023) / 1024) + 1, nblk = nsup * 32;
-    const size_t need = 2 * (nblk + nsup);
-    if (cx->bsum_words < need) {
-        if (cx->bsum) QCK(cudaFree(cx->bsum));
-        cx->bsum = nullptr;
-        cx->bsum_words = 0;
-        QCK(cudaMalloc(&cx->bsum, need * 4));
-        cx->bsum_words = need;
+    for (int g = 0; g < local; ++g) {
+        QRank &k = cx->rk[g];
+        if ((rc = q_rank_alloc(k))) return rc;
+        if (g > 0 && k.cb_words < r.capacity) {     // an emulated rank's replica of the codebook
+            if (k.codebook) QCK(cudaFree(k.codebook));
+            k.codebook = nullptr;
+            k.cb_words = 0;
+            QCK(cudaMalloc(&k.codebook, (size_t)r.capacity * 4));
+            k.cb_words = (size_t)r.capacity;
+        }
+        if ((rc = q_rank_reset(k, r, s, nblk, nsup))) return rc;
     }
-    QCK(cudaMemsetAsync(cx->bsum, 0, need * 4, s));
-    QCK(cudaMemset2DAsync(cx->bsum, 8, 0xff, 4, nblk + nsup, s));
     PArgs a;
     p_fill_args(r, &a);
-    a.bsum = reinterpret_cast<uint2 *>(cx->bsum);
-    a.ssum = reinterpret_cast<uint2 *>(cx->bsum) + nblk;
     a.tabs = cx->tabs;
-    a.surv = cx->surv;
-    a.st = cx->st;
     a.vals = nullptr;
     a.dead = nullptr;
-    a.q = cx->q;
-    a.qdead = cx->qdead; a.qkill = cx->qkill; a.qvals = cx->qvals;
-    a.depth = (int)std::min<uint32_t>(r.opt.pipeline_depth ? r.opt.pipeline_depth : 4u, (uint32_t)kQRing);
-    a.chunk = 2048u;
-    const void *kfn = (const void *)k_pipeline<1>;
+    a.depth = (int)std::min<uint32_t>(r.opt.pipeline_depth ? r.opt.pipeline_depth : 8u, (uint32_t)kQRing);
+    // ranks may run up to 2 x depth tiles apart; a slot is rewritten by a peer only after its
+    // previous tile is committed everywhere when 2 x depth < the ring
+    if (world > 1) a.depth = std::min(a.depth, kQRing / 2 - 1);
+    a.chunk = kQChunk;
+    a.prep_lead = (r.opt.flags & GC_FLAG_NO_PREP) ? 0 : (int)(r.opt.prep_lead ? r.opt.prep_lead : 2u);
+    a.size_on_screen = (r.opt.flags & GC_FLAG_SIZE_ON_TRUE) ? 0 : 1;
+    a.world = world;
+    a.rank = r.world > 1 ? r.rank : 0;
+    for (int g = 0; g < kMaxRanks; ++g) { a.peer_qdead[g] = nullptr; a.peer_flag[g] = nullptr; }
+    for (int g = 0; g < world; ++g) {
+        const bool own = r.world > 1 ? g == r.rank : true;
+        const QRank &k = cx->rk[r.world > 1 ? 0 : g];
+        a.peer_qdead[g] = own ? k.qdead : r.peers->qdead[g];
+        a.peer_flag[g] = own ? k.qflags : r.peers->qflags[g];
+    }
+    const void *kfn = local > 1 ? (const void *)k_pipeline_ranks<1> : (const void *)k_pipeline<1>;
     size_t smem = p_dyn_smem(a.chunk);
     a.nsup_smem = 0;
     if (a.bound) {
@@ -465,25 +806,53 @@ int pipeline_run(const RunArgs &r) {
     int per_sm = 0;
     QCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kPThreads, smem));
     if (per_sm < 1) { set_error("k_pipeline cannot be resident"); return GC_ECUDA; }
-    int grid = cx->sms;
-    if (r.opt.grid_ctas) grid = std::max(2, std::min(grid, (int)r.opt.grid_ctas));   // >= 1 screening CTA
-    const uint32_t screen_warps = (uint32_t)(grid - 1) * kPWarps;
+    int per = cx->sms / local;                       // CTAs per rank in this launch
+    if (r.opt.grid_ctas) per = std::max(2, std::min(per, (int)r.opt.grid_ctas));   // >= 1 screening CTA
+    if (per < 2) { set_error("too many emulated ranks for this GPU"); return GC_EINVAL; }
+    // dedicated preparing CTAs, leaving at least one screening CTA
+    a.prep_ctas = a.prep_lead ? std::min((int)(r.opt.prep_ctas ? r.opt.prep_ctas : 2u), per - 2) : 0;
+    if (a.prep_ctas < 0) a.prep_ctas = 0;
+    const uint32_t screen_warps = (uint32_t)(per - 1 - a.prep_ctas) * kPWarps;
     a.plan_warps = r.opt.plan_warps ? r.opt.plan_warps : std::max<uint32_t>(kPWarps, screen_warps / (uint32_t)a.depth);
-    void *args[] = {&a};
+    PArgs ga[kMaxRanks];
+    for (int g = 0; g < local; ++g) {
+        const QRank &k = cx->rk[g];
+        PArgs &b = ga[g];
+        b = a;
+        if (local > 1) b.rank = g;
+        b.bsum = reinterpret_cast<uint2 *>(k.bsum);
+        b.ssum = reinterpret_cast<uint2 *>(k.bsum) + nblk;
+        b.surv = k.surv;
+        b.st = k.st;
+        b.q = k.q;
+        b.qdead = k.qdead; b.qkill = k.qkill; b.qvals = k.qvals;
+        b.qprep = k.qprep;
+        b.qspill = k.qspill;
+        if (g > 0) { b.codebook = k.codebook; b.d_count = k.count; }
+    }
     QCK(cudaEventRecord(cx->ev0, s));
-    QCK(cudaLaunchCooperativeKernel(kfn, dim3(grid), dim3(kPThreads), args, smem, s));
+    if (local > 1) {
+        QCK(cudaMemcpyAsync(cx->d_args, ga, local * sizeof(PArgs), cudaMemcpyHostToDevice, s));
+        const PArgs *dp = cx->d_args;
+        int ng = local;
+        void *args[] = {&dp, &ng};
+        QCK(cudaLaunchCooperativeKernel(kfn, dim3(per * local), dim3(kPThreads), args, smem, s));
+    } else {
+        void *args[] = {&ga[0]};
+        QCK(cudaLaunchCooperativeKernel(kfn, dim3(per), dim3(kPThreads), args, smem, s));
+    }
     QCK(cudaEventRecord(cx->ev1, s));
     if (r.stats) {
         QCK(cudaStreamSynchronize(s));
         PState h;
-        QCK(cudaMemcpy(&h, cx->st, sizeof(PState), cudaMemcpyDeviceToHost));
+        QCK(cudaMemcpy(&h, cx->rk[0].st, sizeof(PState), cudaMemcpyDeviceToHost));
         QCtl hq;
-        QCK(cudaMemcpy(&hq, cx->q, offsetof(QCtl, slot), cudaMemcpyDeviceToHost));
+        QCK(cudaMemcpy(&hq, cx->rk[0].q, offsetof(QCtl, slot), cudaMemcpyDeviceToHost));
         float ms = 0;
         QCK(cudaEventElapsedTime(&ms, cx->ev0, cx->ev1));
         gc_stats *o = r.stats;
         o->struct_size = sizeof(gc_stats);
-        o->n_ranks = 1;
+        o->n_ranks = (uint32_t)world;
         o->device_ms = ms;
         o->M = h.M;
         o->tiles = h.tiles;
@@ -500,12 +869,24 @@ int pipeline_run(const RunArgs &r) {
         o->resolve_wait_ms = hq.resolve_wait_ns * 1e-6;
         o->resolve_busy_ms = hq.resolve_busy_ns * 1e-6;
         o->pipeline_depth = (uint32_t)a.depth;
+        o->prep_used = hq.prep_used;
+        for (int g = 1; g < local; ++g) {            // emulated ranks: their screen work counts too
+            PState hg;
+            QCK(cudaMemcpy(&hg, cx->rk[g].st, sizeof(PState), cudaMemcpyDeviceToHost));
+            o->checks_exec += hg.checks_exec;
+            o->bound_tests += hg.bound_tests;
+            if (hg.M != h.M) { set_error("emulated ranks disagree on the code size"); return GC_EINTERNAL; }
+        }
         if (a.timing) {
             PState f;
-            QCK(cudaMemcpy(&f, cx->st, sizeof(PState), cudaMemcpyDeviceToHost));
+            QCK(cudaMemcpy(&f, cx->rk[0].st, sizeof(PState), cudaMemcpyDeviceToHost));
             const double T = (double)f.tiles, c = 1965.0;
-            fprintf(stderr, "[gc] pipeline: %llu tiles, depth %d, %.2f us/tile; resolver per tile: wait %.2f busy %.2f us\n",
-                    f.tiles, a.depth, ms * 1e3 / T, hq.resolve_wait_ns / T / 1e3, hq.resolve_busy_ns / T / 1e3);
+            fprintf(stderr, "[gc] pipeline: %llu tiles, %d rank(s), depth %d, prep lead %d (%d CTAs), %.2f us/tile; "
+                    "resolver per tile: wait %.2f busy %.2f us; %llu tiles prepared, %llu resolved from a prep (busy "
+                    "%.2f us each; the others %.2f us each)\n", f.tiles, world, a.depth, a.prep_lead, a.prep_ctas,
+                    ms * 1e3 / T, hq.resolve_wait_ns / T / 1e3, hq.resolve_busy_ns / T / 1e3, hq.preps, hq.prep_used,
+                    hq.busy_prep_ns / 1e3 / (double)std::max(1ull, hq.prep_used),
+                    (hq.resolve_busy_ns - hq.busy_prep_ns) / 1e3 / (double)std::max(1ull, f.tiles - hq.prep_used));
             fprintf(stderr, "[gc]   resolve: gather %.2f conflicts %.2f prior+status %.2f rounds %.2f sequential %.2f "
                     "append %.2f clear+stats %.2f publish %.2f us (SM cycles at 1965 MHz)\n", f.t_r[0] / T / c,
                     f.t_r[1] / T / c, f.t_r[5] / T / c, f.t_r[6] / T / c, f.t_r[2] / T / c, f.t_r[3] / T / c,

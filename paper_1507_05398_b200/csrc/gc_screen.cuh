@@ -14,6 +14,8 @@
 namespace gc {
 
 constexpr int kPThreads = 512;              // threads per CTA (16 warps); grid = #SMs
+constexpr int kMaxRanks = 8;                // ranks of the multi-GPU pipelined engine (one node)
+constexpr int kQRingMax = 16;               // tile slots of the pipelined engine
 constexpr int kPWarps = kPThreads / 32;
 constexpr uint32_t kPR2Min = 1;             // levels with >= this many candidates use 2 per lane
 constexpr uint32_t kPSubMin = 64;           // codewords per warp item: at least ...
@@ -130,6 +132,17 @@ struct PArgs {
     uint32_t *qdead, *qkill, *qvals;   // per ring slot: kPMaxTile/32, kPMaxTile/32 and kPMaxTile words
     int depth;                         // tiles in flight: tile i is screened against codebook[0, M after i - depth)
     uint32_t plan_warps;               // warps the level plans are sized for
+    uint8_t *qprep;                    // per ring slot: p_prep_bytes(chunk) (a prepared tile)
+    uint2 *qspill;                     // per ring slot: kPMaxTile (the preparer's survivors beyond one chunk)
+    int prep_lead;                     // tile i is prepared once tile i - prep_lead is being resolved (0: never)
+    int prep_ctas;                     // CTAs 1 .. prep_ctas only prepare tiles (never screen)
+    int size_on_screen;                // tile sizes bound the survivors of the (older-codebook) screen, which
+                                       // the resolve handles, not only those left after the catch-up checks
+    // multi-rank pipelined engine: the screen of every tile is split over `world` ranks (whole mask
+    // words, gc_tile_partition); every rank resolves the whole tile, so the codebooks stay identical
+    int world, rank;
+    uint32_t *peer_qdead[kMaxRanks];          // each rank's qdead ring: this rank stores its partition's words into all
+    unsigned long long *peer_flag[kMaxRanks]; // each rank's flags [kQRingMax][kMaxRanks]: tile + 1 once rank r's words are in
 };
 
 // Next tile size (a power of two in [tile_min, tile_max]) after a tile of K candidates
@@ -903,35 +916,46 @@ struct PSmem {
     uint32_t tmp_words;
 };
 
-// dead: the tile's dead mask (read, then cleared for the next tile that uses it).
-// prior_lo: survivors are also checked against the committed words codebook[prior_lo, M) --
-//   the pipelined engine screens a tile against an older codebook, codebook[0, prior_lo)
-//   (k_construct: prior_lo = M, nothing to check).
-// On return (thread 0): pc.M / stats updated, pc.S_tile / pc.A_tile / pc.K_used set; the next
-// tile size is the caller's decision.
-__device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsigned long long t0, uint32_t K, int L,
-                                          PCount &pc, PTimers *timer, unsigned long long tm, bool allow_partial,
-                                          uint32_t *dead, unsigned long long prior_lo) {
-    const uint32_t kPChunk = sm.chunk;
-    const uint32_t (*C)[33] = sm.C;
-    const uint64_t *off = sm.off;
-    const uint32_t *s_basis = sm.s_basis;
-    uint32_t *s_ws = sm.s_ws, *s_val = sm.s_val, *s_cnt = sm.s_cnt;
-    uint16_t *s_idx = sm.s_idx;
-    uint8_t *s_status = sm.s_status;
-    uint16_t *s_adj = sm.s_adj;
-    PState *st = a.st;
-    const int lane = threadIdx.x & 31;
-    const uint32_t words = (K + 31) / 32;
-    const uint32_t tid = threadIdx.x;
-    const unsigned long long tg = timer ? clock64() : 0;
-    if (L == 0) {      // empty codebook: no level ran, so the filters are applied here
+// Small scratch of the resolve stages (one static shared-memory allocation per kernel).
+struct RShared {
+    unsigned long long stat[kPWarps][4];
+    uint16_t ovf[kPOvf];
+    uint32_t novf;
+    uint32_t wmin[33];                                       // graded orders: first position of each weight
+    uint32_t gA[kPChunkMaxGroups], gO[kPChunkMaxGroups];     // survivor group consensus (AND / OR of 32)
+    uint32_t qA[kPTmpMaxWords / 32], qO[kPTmpMaxWords / 32]; // staged prior-word blocks
+};
+__device__ __forceinline__ RShared &p_rsh() {
+    __shared__ RShared r;
+    return r;
+}
+
+// A tile prepared off the resolver's critical path (pipelined engine, gc_pipeline.cu): its
+// survivors in rank order, already checked against codebook[.., M_prep), with their in-tile
+// conflict lists -- laid out as the resolve keeps them in shared memory.
+struct PPrep {
+    uint32_t S;                       // survivors stored
+    uint32_t S_screen;                // survivors of the tile's screen (before the preparer's check)
+    unsigned long long M_prep;        // they have no conflict in codebook[0, M_prep)
+    const uint32_t *val, *cnt;        // [S]
+    const uint16_t *idx, *adj;        // [S], [S * kPAdj]
+};
+// per-slot layout of a prepared tile: val u32[chunk], cnt u32[chunk], idx u16[chunk], adj u16[chunk * kPAdj]
+__host__ __device__ constexpr size_t p_prep_bytes(uint32_t chunk) { return (size_t)chunk * (10 + 2 * kPAdj); }
+
+// a3.1 survivors of the tile in rank order (from its dead mask), values regenerated from their
+// ranks (no load): the first `chunk` straight into shared memory (s_idx, s_val), any further ones
+// to `spill` (a.surv for the resolving CTA; null: only counted).  L == 0 (empty codebook, no
+// level ran): the candidate filters are applied here.  Returns S (CTA-uniform).  Ends with a
+// barrier.
+__device__ __forceinline__ uint32_t r_gather(const PArgs &a, const PSmem &sm, unsigned long long t0, uint32_t K,
+                                             int L, uint32_t *dead, uint2 *spill) {
+    const uint32_t tid = threadIdx.x, words = (K + 31) / 32;
+    if (L == 0) {
         for (uint32_t i = tid; i < K; i += blockDim.x)
-            if (!p_allowed(a, p_gen(a, C, off, s_basis, t0 + i))) atomicOr(&dead[i >> 5], 1u << (i & 31));
+            if (!p_allowed(a, p_gen(a, sm.C, sm.off, sm.s_basis, t0 + i))) atomicOr(&dead[i >> 5], 1u << (i & 31));
         __syncthreads();
     }
-    // a3.1 survivors in rank order, values regenerated from their ranks (no load): the first
-    // chunk straight into shared memory, any further ones to a.surv (S <= K)
     uint32_t S = 0;
     for (uint32_t w0 = 0; w0 < words; w0 += blockDim.x) {
         const uint32_t w = w0 + tid;
@@ -941,29 +965,428 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
             if (w * 32 + 32 > K) alive &= (1u << (K - w * 32)) - 1u;
         }
         uint32_t tot;
-        uint32_t pos = S + p_block_scan(__popc(alive), &tot, s_ws);
+        uint32_t pos = S + p_block_scan(__popc(alive), &tot, sm.s_ws);
         while (alive) {
             const int bit = __ffs(alive) - 1;
             alive &= alive - 1;
             const uint32_t i = w * 32 + bit;
-            const uint32_t v = p_gen(a, C, off, s_basis, t0 + i);
-            if (pos < kPChunk) { s_idx[pos] = (uint16_t)i; s_val[pos] = v; }
-            else a.surv[pos] = make_uint2(i, v);
+            const uint32_t v = p_gen(a, sm.C, sm.off, sm.s_basis, t0 + i);
+            if (pos < sm.chunk) { sm.s_idx[pos] = (uint16_t)i; sm.s_val[pos] = v; }
+            else if (spill) spill[pos] = make_uint2(i, v);
             ++pos;
         }
         S += tot;
     }
     __syncthreads();
-    // Partial tile (persistent engine): with more survivors than one chunk, only the candidates
-    // ranked before the first survivor of the second chunk are decided now; the tile is cut
-    // there (K_used) and the rest is screened again as part of the next tile, against a codebook
-    // that then holds this chunk's accepted words.  Exact (tile boundaries never change the
-    // result) and it bounds a resolve to one chunk -- dense early tiles otherwise cost
-    // milliseconds in the multi-chunk path.
+    return S;
+}
+
+// consensus (AND / OR) of every aligned group of 32 survivors s_val[0, Sc).  Ends with a barrier.
+__device__ __forceinline__ void r_consensus(const PSmem &sm, uint32_t Sc) {
+    RShared &r = p_rsh();
+    const int lane = threadIdx.x & 31;
+    const uint32_t ng = (Sc + 31) / 32;
+    for (uint32_t g = threadIdx.x >> 5; g < ng; g += blockDim.x >> 5) {
+        const uint32_t k = 32 * g + lane;
+        const uint32_t x = k < Sc ? sm.s_val[k] : 0u;
+        const uint32_t gA = __reduce_and_sync(0xffffffffu, k < Sc ? x : ~0u);
+        const uint32_t gO = __reduce_or_sync(0xffffffffu, x);
+        if (lane == 0) { r.gA[g] = gA; r.gO[g] = gO; }
+    }
+    __syncthreads();
+}
+
+// a3.2 in-chunk conflicts: one warp task per (group jb of 32 survivors, earlier group kg <= jb):
+// lane t holds survivor 32 jb + t, the survivors of group kg are broadcast by shuffles; a bit
+// mask of the conflicting earlier ones is appended to j's adjacency list (s_adj, up to kPAdj
+// entries, any order; s_cnt[j] > kPAdj marks an overflow).  Two groups whose consensus bound is
+// >= d hold no conflicting pair (not for the orthogonality constraint).  Needs r_consensus.
+// MIX (2..4, distance-only problems): odd columns use the ALU bit-clearing form of the same
+// predicate, so the XU (POPC) and ALU pipes share the work.  Ends with a barrier.
+__device__ __forceinline__ void r_units(const PArgs &a, const PSmem &sm, uint32_t Sc, unsigned long long &rchk) {
+    RShared &r = p_rsh();
+    const int lane = threadIdx.x & 31;
+    for (uint32_t j = threadIdx.x; j < Sc; j += blockDim.x) sm.s_cnt[j] = 0;
+    __syncthreads();
+    const uint32_t ng = (Sc + 31) / 32;
+    auto units = [&](auto so_tag, auto mix_tag) {
+        constexpr bool SO = decltype(so_tag)::value;
+        constexpr int MIXC = decltype(mix_tag)::value;
+        auto cf = [&](uint32_t u, uint32_t w, int t) {
+            if (MIXC >= 2 && (t & 1)) return p_clear_low<MIXC>(u ^ w) == 0u;
+            return (uint32_t)__popc(u ^ w) < a.d || (SO && (__popc(u & w) & 1));
+        };
+        const uint32_t ntask = ng * (ng + 1) / 2;
+        for (uint32_t p = threadIdx.x >> 5; p < ntask; p += blockDim.x >> 5) {
+            uint32_t jb = (uint32_t)((sqrtf(8.0f * (float)p + 1.0f) - 1.0f) * 0.5f);
+            while ((jb + 1) * (jb + 2) / 2 <= p) ++jb;
+            while (jb * (jb + 1) / 2 > p) --jb;
+            const uint32_t kg = p - jb * (jb + 1) / 2;
+            const uint32_t j = 32 * jb + lane, k = 32 * kg + lane;
+            if (!SO && p_lb(r.gA[jb], r.gO[jb], r.gA[kg], r.gO[kg], a.nmask) >= a.d) continue;
+            const uint32_t vj = j < Sc ? sm.s_val[j] : 0u, vk = k < Sc ? sm.s_val[k] : 0u;
+            uint32_t mask = 0;
+#pragma unroll
+            for (int t = 0; t < 32; ++t) mask |= (uint32_t)cf(vj, __shfl_sync(0xffffffffu, vk, t), t) << t;
+            const uint32_t kmax = min(j, Sc);                 // earlier survivors only
+            const uint32_t lim = kmax > 32 * kg ? min(32u, kmax - 32 * kg) : 0u;
+            mask &= lim >= 32 ? 0xffffffffu : ((1u << lim) - 1u);
+            if (j < Sc) rchk += lim;
+            if (j < Sc && mask) {
+                uint32_t q = atomicAdd(&sm.s_cnt[j], (uint32_t)__popc(mask));
+                while (mask) {
+                    const uint32_t t = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    if (q < kPAdj) sm.s_adj[j * kPAdj + q] = (uint16_t)(32 * kg + t);
+                    ++q;
+                }
+            }
+        }
+    };
+    if (a.so) units(std::true_type{}, std::integral_constant<int, 0>{});
+    else if (a.mix == 2) units(std::false_type{}, std::integral_constant<int, 2>{});
+    else if (a.mix == 3) units(std::false_type{}, std::integral_constant<int, 3>{});
+    else if (a.mix == 4) units(std::false_type{}, std::integral_constant<int, 4>{});
+    else units(std::false_type{}, std::integral_constant<int, 0>{});
+    __syncthreads();
+}
+
+// v in conflict with one of the words w[0, e) (shared memory, the same address in every lane):
+// distance < d, or (SO) odd AND-parity.  A full block of 32 is read four words per 128-bit
+// broadcast load, fully unrolled; with MIX (2..4) odd words use the ALU bit-clearing form of the
+// distance test so that the POPC and ALU pipes share the work.
+template <bool SO, int MIX>
+__device__ __forceinline__ bool r_hit(uint32_t v, const uint32_t *w, uint32_t e, uint32_t d) {
+    uint32_t m = 0xffffffffu;
+    bool hit = false;
+    if (e == 32) {
+        const uint4 *w4 = reinterpret_cast<const uint4 *>(w);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint4 c = w4[k];
+            const uint32_t cs[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (SO) hit |= (__popc(v & cs[u]) & 1) != 0;
+                if (MIX >= 2 && (u & 1)) hit |= p_clear_low<MIX>(v ^ cs[u]) == 0u;
+                else m = min(m, (uint32_t)__popc(v ^ cs[u]));
+            }
+        }
+    } else {
+        for (uint32_t t = 0; t < e; ++t) {
+            const uint32_t c = w[t];
+            if (SO) hit |= (__popc(v & c) & 1) != 0;
+            m = min(m, (uint32_t)__popc(v ^ c));
+        }
+    }
+    return hit || m < d;
+}
+
+// Survivors s_val[0, Sc) against committed words codebook[lo, hi) the screen did not see:
+// s_status[j] |= 1 on a conflict (zeroed first unless `accumulate`).  The words are staged
+// through shared memory newest first; a warp task is (group of 32 survivors, block of 32 staged
+// words), skipped when the consensus bound of the two is >= d.  Needs r_consensus.  Ends with a
+// barrier.
+// first_loaded: the newest batch, codebook[hi - min(tmp_words, hi - lo), hi), is already in s_tmp.
+__device__ __forceinline__ void r_prior(const PArgs &a, const PSmem &sm, uint32_t Sc, unsigned long long lo,
+                                        unsigned long long hi, bool accumulate, unsigned long long &rchk,
+                                        bool first_loaded = false) {
+    RShared &r = p_rsh();
+    const int lane = threadIdx.x & 31;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t ng = (Sc + 31) / 32;
+    if (!accumulate)
+        for (uint32_t j = tid; j < Sc; j += blockDim.x) sm.s_status[j] = 0;
+    for (unsigned long long top = hi; top > lo;) {
+        const uint32_t nb = (uint32_t)min((unsigned long long)sm.tmp_words, top - lo);
+        const unsigned long long b0 = top - nb;
+        __syncthreads();
+        if (!first_loaded || top != hi)
+            for (uint32_t t = tid; t < nb; t += blockDim.x) sm.s_tmp[t] = __ldcg(a.codebook + b0 + t);
+        __syncthreads();
+        const uint32_t nq = (nb + 31) / 32;
+        for (uint32_t q = tid >> 5; q < nq; q += blockDim.x >> 5) {
+            const uint32_t k = 32 * q + lane;
+            const uint32_t x = k < nb ? sm.s_tmp[k] : 0u;
+            const uint32_t qA = __reduce_and_sync(0xffffffffu, k < nb ? x : ~0u);
+            const uint32_t qO = __reduce_or_sync(0xffffffffu, x);
+            if (lane == 0) { r.qA[q] = qA; r.qO[q] = qO; }
+        }
+        __syncthreads();
+        const uint32_t ntask = ng * nq;
+        auto tasks = [&](auto so_tag, auto mix_tag) {
+            constexpr bool SO = decltype(so_tag)::value;
+            constexpr int MIX = decltype(mix_tag)::value;
+            for (uint32_t p = tid >> 5; p < ntask; p += blockDim.x >> 5) {
+                const uint32_t g = p / nq, q = p - g * nq;
+                if (!SO && p_lb(r.gA[g], r.gO[g], r.qA[q], r.qO[q], a.nmask) >= a.d) continue;
+                const uint32_t j = 32 * g + lane;
+                const uint32_t vj = j < Sc ? sm.s_val[j] : 0u;
+                const uint32_t e = min(32u, nb - 32 * q);
+                const bool c = r_hit<SO, MIX>(vj, sm.s_tmp + 32 * q, e, a.d);
+                if (j < Sc) {
+                    rchk += e;
+                    if (c) sm.s_status[j] = 1;
+                }
+            }
+        };
+        if (a.so) tasks(std::true_type{}, std::integral_constant<int, 0>{});
+        else if (a.mix == 2) tasks(std::false_type{}, std::integral_constant<int, 2>{});
+        else if (a.mix == 3) tasks(std::false_type{}, std::integral_constant<int, 3>{});
+        else if (a.mix == 4) tasks(std::false_type{}, std::integral_constant<int, 4>{});
+        else tasks(std::false_type{}, std::integral_constant<int, 0>{});
+        top = b0;
+    }
+    __syncthreads();
+}
+
+// Stable compaction of the chunk s_val / s_idx [0, Sc) to the survivors with s_status == 0 (no
+// conflict with a committed word), in place: a round reads its elements before any of them is
+// overwritten and writes only below its own range.  Returns the count (CTA-uniform).  Ends with
+// a barrier.
+__device__ __forceinline__ uint32_t r_compact(const PSmem &sm, uint32_t Sc) {
+    uint32_t out = 0;
+    for (uint32_t j0 = 0; j0 < Sc; j0 += blockDim.x) {
+        const uint32_t j = j0 + threadIdx.x;
+        const bool keep = j < Sc && sm.s_status[j] == 0;
+        const uint32_t v = keep ? sm.s_val[j] : 0u;
+        const uint16_t ix = keep ? sm.s_idx[j] : (uint16_t)0;
+        uint32_t tot;
+        const uint32_t pos = out + p_block_scan(keep ? 1u : 0u, &tot, sm.s_ws);   // has barriers
+        if (keep) { sm.s_val[pos] = v; sm.s_idx[pos] = ix; }
+        out += tot;
+        __syncthreads();
+    }
+    return out;
+}
+
+// a3.3 decide the chunk s_val[0, Sc) in rank order: s_status = 1 accepted / 0 rejected.
+// On entry s_cnt / s_adj hold the in-chunk conflict lists and, when `prior`, s_status[j] != 0
+// marks a survivor with a conflict outside the chunk (rejected outright; counted in pkill).
+// Parallel rounds: an undecided survivor is rejected as soon as one earlier conflicting survivor
+// is accepted, accepted once all of them are rejected; long chains are finished by warp 0 in
+// rank order.  A survivor is accepted iff no earlier ACCEPTED survivor conflicts.
+// Survivors with more than kPAdj earlier conflicts ("overflow") are listed (up to kPOvf) and
+// decided by a whole warp per node.  Ends with a barrier.
+__device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32_t Sc, bool prior,
+                                         unsigned long long &confl, unsigned long long &pkill, PTimers *timer,
+                                         unsigned long long &tr) {
+    RShared &r = p_rsh();
+    PState *st = a.st;
+    const int lane = threadIdx.x & 31;
+    const uint32_t tid = threadIdx.x;
+    uint8_t *s_status = sm.s_status;
+    const uint32_t *s_val = sm.s_val;
+    uint32_t *s_cnt = sm.s_cnt;
+    const uint16_t *s_adj = sm.s_adj;
+    if (tid == 0) r.novf = 0;
+    __syncthreads();
+    for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+        const bool prev = prior && s_status[j] != 0;
+        const uint32_t cnt = s_cnt[j];
+        s_status[j] = prev ? 0 : (cnt ? 2 : 1);
+        confl += cnt;
+        pkill += prev;
+        if (cnt > kPAdj) {
+            if (a.timing) atomicAdd(&st->n_overflow, 1ull);
+            if (!prev) {
+                const uint32_t o = atomicAdd(&r.novf, 1u);
+                if (o < kPOvf) { r.ovf[o] = (uint16_t)j; s_cnt[j] = kPOvfMark; }
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t novf = min(r.novf, kPOvf);
+    if (timer) { const unsigned long long t_ = clock64(); timer->r[5] += t_ - tr; tr = t_; }
+    int left = 0;
+    for (int round = 0; round < 8; ++round) {
+        int undecided = 0;
+        for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+            if (s_status[j] != 2) continue;
+            const uint32_t cn = s_cnt[j];
+            if (cn == kPOvfMark) { undecided = 1; continue; }     // a warp decides it below
+            bool acc_nb = false, und_nb = false;
+            if (cn <= kPAdj) {
+                for (uint32_t t = 0; t < cn; ++t) {
+                    const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
+                    acc_nb |= sk == 1;
+                    und_nb |= sk == 2;
+                }
+            } else {
+                const uint32_t vj = s_val[j];
+                for (uint32_t k = 0; k < j; ++k) {
+                    if (p_conflict(a, vj, s_val[k])) {
+                        const uint8_t sk = s_status[k];
+                        acc_nb |= sk == 1;
+                        und_nb |= sk == 2;
+                    }
+                }
+            }
+            // a status read in the same round may be stale (2): that only delays
+            if (acc_nb) s_status[j] = 0;
+            else if (!und_nb) s_status[j] = 1;
+            else undecided = 1;
+        }
+        for (uint32_t o = tid >> 5; o < novf; o += blockDim.x >> 5) {
+            const uint32_t j = r.ovf[o];
+            if (s_status[j] != 2) continue;                       // warp-uniform
+            const uint32_t vj = s_val[j];
+            bool acc_nb = false, und_nb = false;
+            for (uint32_t k = lane; k < j; k += 32) {
+                if (p_conflict(a, vj, s_val[k])) {
+                    const uint8_t sk = s_status[k];
+                    acc_nb |= sk == 1;
+                    und_nb |= sk == 2;
+                }
+            }
+            acc_nb = __any_sync(0xffffffffu, acc_nb);
+            und_nb = __any_sync(0xffffffffu, und_nb);
+            if (lane == 0) {
+                if (acc_nb) s_status[j] = 0;
+                else if (!und_nb) s_status[j] = 1;
+            }
+        }
+        if (a.timing && tid == 0) {
+            atomicAdd(&st->n_rounds, 1ull);
+            atomicMax(&st->n_rounds_max, (unsigned long long)round + 1);
+        }
+        left = __syncthreads_or(undecided);
+        if (!left) break;
+    }
+    if (timer) { const unsigned long long t_ = clock64(); timer->r[6] += t_ - tr; tr = t_; }
+    if (left && tid < 32) {
+        for (uint32_t j = 0; j < Sc; ++j) {
+            if (s_status[j] != 2) continue;                 // warp-uniform
+            if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
+            const uint32_t cn = s_cnt[j];
+            bool acc_nb = false;
+            if (cn <= kPAdj) {
+                if (lane < cn) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
+            } else {
+                const uint32_t vj = s_val[j];
+                for (uint32_t k = lane; k < j; k += 32)
+                    acc_nb |= (s_status[k] == 1) && p_conflict(a, vj, s_val[k]);
+            }
+            acc_nb = __any_sync(0xffffffffu, acc_nb);
+            if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (timer) { const unsigned long long t_ = clock64(); timer->r[2] += t_ - tr; tr = t_; }
+}
+
+// a4 ordered append of the chunk's accepted survivors at codebook[M0 + A, ...); their values are
+// also staged in order (in s_adj, free now) for the block-bound summaries: AND / OR per aligned
+// block of 32 (a warp covers one block) and per super-block of 1024 -- appends only ever narrow
+// the AND and widen the OR; fire-and-forget atomics published by the commit's release.
+// Returns the new A (CTA-uniform).  Ends with a barrier.
+__device__ __forceinline__ uint32_t r_append(const PArgs &a, const PSmem &sm, uint32_t Sc, unsigned long long M0,
+                                             uint32_t A, unsigned long long t0, unsigned long long &wdef) {
+    RShared &r = p_rsh();
+    PState *st = a.st;
+    const int lane = threadIdx.x & 31;
+    const uint32_t tid = threadIdx.x;
+    uint32_t *s_stage = reinterpret_cast<uint32_t *>(sm.s_adj);
+    const uint32_t A_start = A;
+    for (uint32_t j0 = 0; j0 < Sc; j0 += blockDim.x) {
+        const uint32_t j = j0 + tid;
+        const uint32_t acc = (j < Sc && sm.s_status[j] == 1) ? 1u : 0u;
+        uint32_t tot;
+        const uint32_t pos = A + p_block_scan(acc, &tot, sm.s_ws);
+        if (acc) {
+            const unsigned long long p = M0 + pos;
+            const uint32_t v = sm.s_val[j];
+            s_stage[pos - A_start] = v;
+            if (a.weight_bound) atomicMin(&r.wmin[__popc(v)], pos);
+            if (p < a.capacity) {
+                a.codebook[p] = v;
+            } else {
+                st->error = 1;
+            }
+            if (a.wdef_valid) wdef += a.N - 1 - (t0 + sm.s_idx[j]);
+        }
+        A += tot;
+    }
+    __syncthreads();
+    if (a.bound && A > A_start) {
+        const unsigned long long b = M0 + A_start, e = min(M0 + A, (unsigned long long)a.capacity);
+        const unsigned long long p0 = b & ~31ull;
+        for (unsigned long long p = p0 + tid; p < ((e + 31) & ~31ull); p += blockDim.x) {
+            const bool in = p >= b && p < e;
+            const uint32_t w = in ? s_stage[p - b] : 0u;
+            const uint32_t an = __reduce_and_sync(0xffffffffu, in ? w : ~0u);
+            const uint32_t orr = __reduce_or_sync(0xffffffffu, w);
+            if (lane == 0) {
+                atomicAnd(&a.bsum[p >> 5].x, an);
+                atomicOr(&a.bsum[p >> 5].y, orr);
+                atomicAnd(&a.ssum[p >> 10].x, an);
+                atomicOr(&a.ssum[p >> 10].y, orr);
+            }
+        }
+    }
+    if (A > a.capacity - M0) A = (uint32_t)(a.capacity - M0);
+    __threadfence_block();
+    __syncthreads();
+    return A;
+}
+
+// a3 + a4 for one tile, by ONE CTA: survivors in rank order (from the dead mask), in-tile
+// ordered resolve, ordered append, M += A, next tile size, per-tile state cleared.
+// dead: the tile's dead mask (read, then cleared for the next tile that uses it).
+// prior_lo: survivors are also checked against the committed words codebook[prior_lo, M) --
+//   the pipelined engine screens a tile against an older codebook, codebook[0, prior_lo)
+//   (k_construct: prior_lo = M, nothing to check).
+// prep (pipelined engine, may be null): the tile's survivors were gathered, checked against
+//   codebook[prior_lo, prep->M_prep) and their conflict lists built by another CTA; they are
+//   loaded instead, and only codebook[prep->M_prep, M) remains to be checked.
+// On return (thread 0): pc.M / stats updated, pc.S_tile (survivors without a committed
+// conflict) / pc.A_tile / pc.K_used set; the next tile size is the caller's decision.
+__device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsigned long long t0, uint32_t K, int L,
+                                          PCount &pc, PTimers *timer, unsigned long long tm, bool allow_partial,
+                                          uint32_t *dead, unsigned long long prior_lo, const PPrep *prep = nullptr) {
+    const uint32_t kPChunk = sm.chunk;
+    PState *st = a.st;
+    RShared &r = p_rsh();
+    const int lane = threadIdx.x & 31;
+    const uint32_t words = (K + 31) / 32;
+    const uint32_t tid = threadIdx.x;
+    const unsigned long long tg = timer ? clock64() : 0;
+    uint32_t S;
+    bool pre_loaded = false;
+    if (prep) {
+        S = prep->S;
+        prior_lo = prep->M_prep;
+        // one round trip: the prepared survivors and the newest committed words they still have to
+        // be checked against (r_prior's first batch)
+        const unsigned long long M0 = pc.M;
+        if (M0 > prior_lo && S > 0) {
+            const uint32_t nb = (uint32_t)min((unsigned long long)sm.tmp_words, M0 - prior_lo);
+            for (uint32_t t = tid; t < nb; t += blockDim.x) sm.s_tmp[t] = __ldcg(a.codebook + M0 - nb + t);
+            pre_loaded = true;
+        }
+        for (uint32_t j = tid; j < S; j += blockDim.x) {
+            sm.s_val[j] = __ldcg(prep->val + j);
+            sm.s_cnt[j] = __ldcg(prep->cnt + j);
+            sm.s_idx[j] = __ldcg(prep->idx + j);
+        }
+        const uint4 *src = reinterpret_cast<const uint4 *>(prep->adj);
+        uint4 *dst = reinterpret_cast<uint4 *>(sm.s_adj);
+        for (uint32_t q = tid; q < S * (kPAdj / 8); q += blockDim.x) dst[q] = __ldcg(src + q);
+        __syncthreads();
+    } else {
+        S = r_gather(a, sm, t0, K, L, dead, a.surv);
+    }
+    const uint32_t S_screen = prep ? prep->S_screen : S;
+    // Partial tile (k_construct): with more survivors than one chunk, only the candidates ranked
+    // before the first survivor of the second chunk are decided now; the tile is cut there
+    // (K_used) and the rest is screened again as part of the next tile, against a codebook that
+    // then holds this chunk's accepted words.  Exact (tile boundaries never change the result)
+    // and it bounds a resolve to one chunk.
     uint32_t K_used = K;
     const uint32_t s_cut = min(kPChunk, a.partial_s);
-    if (allow_partial && S > s_cut) {
-        K_used = s_cut < kPChunk ? s_idx[s_cut] : __ldcg(&a.surv[kPChunk].x);
+    if (!prep && allow_partial && S > s_cut) {
+        K_used = s_cut < kPChunk ? sm.s_idx[s_cut] : __ldcg(&a.surv[kPChunk].x);
         S = s_cut;
     }
     // resolve sub-steps timed with the SM cycle counter (one CTA: consistent, and cheap to read)
@@ -974,283 +1397,56 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         atomicMax(&st->s_max, (unsigned long long)S);
         if (S > kPChunk) atomicAdd(&st->n_chunked, 1ull);
     }
-    __shared__ unsigned long long s_stat[kPWarps][3];
-    __shared__ uint16_t s_ovf[kPOvf];
-    __shared__ uint32_t s_novf;
-    __shared__ uint32_t s_wmin[33];          // graded orders: first tile position of each weight
-    __shared__ uint32_t s_gA[kPChunkMaxGroups], s_gO[kPChunkMaxGroups];   // survivor group consensus
-    __shared__ uint32_t s_qA[kPTmpMaxWords / 32], s_qO[kPTmpMaxWords / 32];  // staged prior-word blocks
-    if (tid < 33) s_wmin[tid] = 0xffffffffu;
-    unsigned long long rchk = 0, confl = 0, wdef = 0;
+    if (tid < 33) r.wmin[tid] = 0xffffffffu;
+    unsigned long long rchk = 0, confl = 0, wdef = 0, pkill = 0;
     const unsigned long long M0 = pc.M;
     uint32_t A = 0;                   // accepted so far in this tile (codebook[M0, M0+A))
     for (uint32_t c0 = 0; c0 < S; c0 += kPChunk) {
-        const uint32_t Sc = min(kPChunk, S - c0);
+        uint32_t Sc = min(kPChunk, S - c0);
         if (c0 > 0) {
             for (uint32_t j = tid; j < Sc; j += blockDim.x) {
                 const uint2 e = __ldcg(a.surv + c0 + j);
-                s_idx[j] = (uint16_t)e.x;
-                s_val[j] = e.y;
+                sm.s_idx[j] = (uint16_t)e.x;
+                sm.s_val[j] = e.y;
             }
         }
-        for (uint32_t j = tid; j < Sc; j += blockDim.x) s_cnt[j] = 0;
         __syncthreads();
-        // a3.2 in-chunk conflicts, one work unit per (survivor j, aligned group of 32 earlier
-        // survivors): a bit mask of the conflicting ones, appended to j's adjacency list
-        // (s_adj, up to kPAdj entries, any order; s_cnt[j] > kPAdj marks an overflow)
-        const uint32_t ng = (Sc + 31) / 32;
-        // group consensus (AND / OR of 32 survivors) for the bound between two groups
-        for (uint32_t g = tid >> 5; g < ng; g += blockDim.x >> 5) {
-            const uint32_t k = 32 * g + lane;
-            const uint32_t x = k < Sc ? s_val[k] : 0u;
-            const uint32_t gA = __reduce_and_sync(0xffffffffu, k < Sc ? x : ~0u);
-            const uint32_t gO = __reduce_or_sync(0xffffffffu, x);
-            if (lane == 0) { s_gA[g] = gA; s_gO[g] = gO; }
-        }
-        __syncthreads();
-        // MIX (2..4, distance-only problems): odd columns use the ALU bit-clearing form of the
-        // same predicate, so the XU (POPC) and ALU pipes share the one SM's work
-        auto units = [&](auto so_tag, auto mix_tag) {
-            constexpr bool SO = decltype(so_tag)::value;
-            constexpr int MIXC = decltype(mix_tag)::value;
-            auto cf = [&](uint32_t u, uint32_t w, int t) {
-                if (MIXC >= 2 && (t & 1)) return p_clear_low<MIXC>(u ^ w) == 0u;
-                return (uint32_t)__popc(u ^ w) < a.d || (SO && (__popc(u & w) & 1));
-            };            // warp task p = block pair (jb, kg <= jb): lane t holds survivor 32 jb + t, the 32
-            // survivors of group kg are broadcast by shuffles (no division, no idle lanes but on
-            // the diagonal)
-            const uint32_t ntask = ng * (ng + 1) / 2;
-            for (uint32_t p = tid >> 5; p < ntask; p += blockDim.x >> 5) {
-                uint32_t jb = (uint32_t)((sqrtf(8.0f * (float)p + 1.0f) - 1.0f) * 0.5f);
-                while ((jb + 1) * (jb + 2) / 2 <= p) ++jb;
-                while (jb * (jb + 1) / 2 > p) --jb;
-                const uint32_t kg = p - jb * (jb + 1) / 2;
-                const uint32_t j = 32 * jb + lane, k = 32 * kg + lane;
-                // two groups whose consensus bound is >= d hold no conflicting pair (not for the
-                // orthogonality constraint)
-                if (!SO && p_lb(s_gA[jb], s_gO[jb], s_gA[kg], s_gO[kg], a.nmask) >= a.d) continue;
-                const uint32_t vj = j < Sc ? s_val[j] : 0u, vk = k < Sc ? s_val[k] : 0u;
-                uint32_t mask = 0;
-#pragma unroll
-                for (int t = 0; t < 32; ++t) mask |= (uint32_t)cf(vj, __shfl_sync(0xffffffffu, vk, t), t) << t;
-                const uint32_t kmax = min(j, Sc);                 // earlier survivors only
-                const uint32_t lim = kmax > 32 * kg ? min(32u, kmax - 32 * kg) : 0u;
-                mask &= lim >= 32 ? 0xffffffffu : ((1u << lim) - 1u);
-                if (j < Sc) rchk += lim;
-                if (j < Sc && mask) {
-                    uint32_t q = atomicAdd(&s_cnt[j], (uint32_t)__popc(mask));
-                    while (mask) {
-                        const uint32_t t = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        if (q < kPAdj) s_adj[j * kPAdj + q] = (uint16_t)(32 * kg + t);
-                        ++q;
-                    }
-                }
-            }
-        };
-        if (a.so) units(std::true_type{}, std::integral_constant<int, 0>{});
-        else if (a.mix == 2) units(std::false_type{}, std::integral_constant<int, 2>{});
-        else if (a.mix == 3) units(std::false_type{}, std::integral_constant<int, 3>{});
-        else if (a.mix == 4) units(std::false_type{}, std::integral_constant<int, 4>{});
-        else units(std::false_type{}, std::integral_constant<int, 0>{});
-        __syncthreads();
-        // status: 1 = accepted, 0 = rejected, 2 = undecided.  A survivor conflicting with a word
-        // accepted in an earlier chunk of this tile is rejected outright (multi-chunk tiles only).
-        P_TR(1)
-        // Survivors with more than kPAdj earlier conflicts ("overflow") are listed in s_ovf (up to
-        // kPOvf; s_cnt = kPOvfMark) and decided by a whole warp per node in the rounds below.
-        if (tid == 0) s_novf = 0;
-        __syncthreads();
-        const unsigned long long Mc = M0 + A;           // committed words + this tile's earlier chunks
-        const bool prior = Mc > prior_lo;
-        if (prior) {
-            // A survivor conflicting with a committed word the screen did not see is rejected:
+        r_consensus(sm, Sc);
+        const bool pc_prior = M0 > prior_lo, ch_prior = A > 0;
+        if (prep) {
+            // the preparer built the conflict lists; the committed words it did not see only flag
+            if (pc_prior) r_prior(a, sm, Sc, prior_lo, M0, false, rchk, pre_loaded);
+            P_TR(1)
+            r_decide(a, sm, Sc, pc_prior, confl, pkill, timer, tr);
+        } else {
+            // Survivors conflicting with a committed word the screen did not see are rejected first:
             // codebook[prior_lo, M0) (pipelined engine: the tile was screened against an older
-            // codebook) and [M0, M0 + A) (words accepted in this tile's earlier chunks).  They are
-            // staged through shared memory newest first; a warp task is (group of 32 survivors,
-            // block of 32 staged words), skipped when the consensus bound of the two is >= d;
-            // s_status holds the verdict (1 = conflict) until the status pass below.
-            for (uint32_t j = tid; j < Sc; j += blockDim.x) s_status[j] = 0;
-            for (unsigned long long top = Mc; top > prior_lo;) {
-                const uint32_t nb = (uint32_t)min((unsigned long long)sm.tmp_words, top - prior_lo);
-                const unsigned long long b0 = top - nb;
-                __syncthreads();
-                for (uint32_t t = tid; t < nb; t += blockDim.x) sm.s_tmp[t] = __ldcg(a.codebook + b0 + t);
-                __syncthreads();
-                const uint32_t nq = (nb + 31) / 32;
-                for (uint32_t q = tid >> 5; q < nq; q += blockDim.x >> 5) {
-                    const uint32_t k = 32 * q + lane;
-                    const uint32_t x = k < nb ? sm.s_tmp[k] : 0u;
-                    const uint32_t qA = __reduce_and_sync(0xffffffffu, k < nb ? x : ~0u);
-                    const uint32_t qO = __reduce_or_sync(0xffffffffu, x);
-                    if (lane == 0) { s_qA[q] = qA; s_qO[q] = qO; }
+            // codebook) and [M0, M0 + A) (words accepted in this tile's earlier chunks).  The rest
+            // is compacted and only it gets in-tile conflict lists.  The first kind also leaves the
+            // survivor count the tile size is chosen from (pkill).
+            if (pc_prior || ch_prior) {
+                if (pc_prior) r_prior(a, sm, Sc, prior_lo, M0, false, rchk, pre_loaded);
+                if (ch_prior) {
+                    if (pc_prior)
+                        for (uint32_t j = tid; j < Sc; j += blockDim.x) pkill += sm.s_status[j] != 0;
+                    r_prior(a, sm, Sc, M0, M0 + A, pc_prior, rchk);
                 }
-                __syncthreads();
-                const uint32_t ntask = ng * nq;
-                for (uint32_t p = tid >> 5; p < ntask; p += blockDim.x >> 5) {
-                    const uint32_t g = p / nq, q = p - g * nq;
-                    if (!a.so && p_lb(s_gA[g], s_gO[g], s_qA[q], s_qO[q], a.nmask) >= a.d) continue;
-                    const uint32_t j = 32 * g + lane;
-                    const uint32_t vj = j < Sc ? s_val[j] : 0u;
-                    const uint32_t e = min(32u, nb - 32 * q);
-                    bool c = false;
-                    for (uint32_t t = 0; t < e; ++t) c |= p_conflict(a, vj, sm.s_tmp[32 * q + t]);
-                    if (j < Sc) {
-                        rchk += e;
-                        if (c) s_status[j] = 1;
-                    }
-                }
-                top = b0;
+                const uint32_t Sc2 = r_compact(sm, Sc);
+                if (pc_prior && !ch_prior && tid == 0) pkill += Sc - Sc2;
+                Sc = Sc2;
+                r_consensus(sm, Sc);
             }
-            __syncthreads();
+            r_units(a, sm, Sc, rchk);
+            P_TR(1)
+            unsigned long long none = 0;
+            r_decide(a, sm, Sc, false, confl, none, timer, tr);
         }
-        for (uint32_t j = tid; j < Sc; j += blockDim.x) {
-            const bool prev = prior && s_status[j] != 0;
-            const uint32_t cnt = s_cnt[j];
-            s_status[j] = prev ? 0 : (cnt ? 2 : 1);
-            confl += cnt;
-            if (cnt > kPAdj) {
-                if (a.timing) atomicAdd(&st->n_overflow, 1ull);
-                if (!prev) {
-                    const uint32_t o = atomicAdd(&s_novf, 1u);
-                    if (o < kPOvf) { s_ovf[o] = (uint16_t)j; s_cnt[j] = kPOvfMark; }
-                }
-            }
-        }
-        __syncthreads();
-        const uint32_t novf = min(s_novf, kPOvf);
-        P_TR(5)
-        // a3.3 parallel rounds: an undecided survivor is rejected as soon as one earlier
-        // conflicting survivor is accepted, accepted once all of them are rejected.  Long
-        // dependency chains are finished by warp 0 walking the undecided ones in rank order.
-        // A survivor is accepted iff no earlier ACCEPTED survivor conflicts.
-        int left = 0;
-        for (int round = 0; round < 8; ++round) {
-            int undecided = 0;
-            for (uint32_t j = tid; j < Sc; j += blockDim.x) {
-                if (s_status[j] != 2) continue;
-                const uint32_t cn = s_cnt[j];
-                if (cn == kPOvfMark) { undecided = 1; continue; }     // a warp decides it below
-                bool acc_nb = false, und_nb = false;
-                if (cn <= kPAdj) {
-                    for (uint32_t t = 0; t < cn; ++t) {
-                        const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
-                        acc_nb |= sk == 1;
-                        und_nb |= sk == 2;
-                    }
-                } else {
-                    const uint32_t vj = s_val[j];
-                    for (uint32_t k = 0; k < j; ++k) {
-                        if (p_conflict(a, vj, s_val[k])) {
-                            const uint8_t sk = s_status[k];
-                            acc_nb |= sk == 1;
-                            und_nb |= sk == 2;
-                        }
-                    }
-                }
-                // a status read in the same round may be stale (2): that only delays
-                if (acc_nb) s_status[j] = 0;
-                else if (!und_nb) s_status[j] = 1;
-                else undecided = 1;
-            }
-            // listed overflow nodes: lanes scan the earlier survivors
-            for (uint32_t o = tid >> 5; o < novf; o += blockDim.x >> 5) {
-                const uint32_t j = s_ovf[o];
-                if (s_status[j] != 2) continue;                       // warp-uniform
-                const uint32_t vj = s_val[j];
-                bool acc_nb = false, und_nb = false;
-                for (uint32_t k = lane; k < j; k += 32) {
-                    if (p_conflict(a, vj, s_val[k])) {
-                        const uint8_t sk = s_status[k];
-                        acc_nb |= sk == 1;
-                        und_nb |= sk == 2;
-                    }
-                }
-                acc_nb = __any_sync(0xffffffffu, acc_nb);
-                und_nb = __any_sync(0xffffffffu, und_nb);
-                if (lane == 0) {
-                    if (acc_nb) s_status[j] = 0;
-                    else if (!und_nb) s_status[j] = 1;
-                }
-            }
-            if (a.timing && tid == 0) {
-                atomicAdd(&st->n_rounds, 1ull);
-                atomicMax(&st->n_rounds_max, (unsigned long long)round + 1);
-            }
-            left = __syncthreads_or(undecided);
-            if (!left) break;
-        }
-        P_TR(6)
-        if (left && tid < 32) {
-            for (uint32_t j = 0; j < Sc; ++j) {
-                if (s_status[j] != 2) continue;                 // warp-uniform
-                if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
-                const uint32_t cn = s_cnt[j];
-                bool acc_nb = false;
-                if (cn <= kPAdj) {
-                    if (lane < cn) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
-                } else {
-                    const uint32_t vj = s_val[j];
-                    for (uint32_t k = lane; k < j; k += 32)
-                        acc_nb |= (s_status[k] == 1) && p_conflict(a, vj, s_val[k]);
-                }
-                acc_nb = __any_sync(0xffffffffu, acc_nb);
-                if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
-                __syncwarp();
-            }
-        }
-        __syncthreads();
-        P_TR(2)
-        // a4 ordered append of the chunk's accepted survivors; their values are also staged in
-        // order (in s_adj, free now) for the block-bound summaries
-        uint32_t *s_stage = reinterpret_cast<uint32_t *>(s_adj);
-        const uint32_t A_start = A;
-        for (uint32_t j0 = 0; j0 < Sc; j0 += blockDim.x) {
-            const uint32_t j = j0 + tid;
-            const uint32_t acc = (j < Sc && s_status[j] == 1) ? 1u : 0u;
-            uint32_t tot;
-            const uint32_t pos = A + p_block_scan(acc, &tot, s_ws);
-            if (acc) {
-                const unsigned long long p = M0 + pos;
-                const uint32_t v = s_val[j];
-                s_stage[pos - A_start] = v;
-                if (a.weight_bound) atomicMin(&s_wmin[__popc(v)], pos);
-                if (p < a.capacity) {
-                    a.codebook[p] = v;
-                } else {
-                    st->error = 1;
-                }
-                if (a.wdef_valid) wdef += a.N - 1 - (t0 + s_idx[j]);
-            }
-            A += tot;
-        }
-        __syncthreads();
-        if (a.bound && A > A_start) {
-            // AND / OR per aligned block of 32 (warp w of the loop covers one block) and per
-            // super-block of 1024; appends only ever narrow the AND and widen the OR.  The
-            // reductions are fire-and-forget; the grid barrier after the commit publishes them.
-            const unsigned long long b = M0 + A_start, e = min(M0 + A, (unsigned long long)a.capacity);
-            const unsigned long long p0 = b & ~31ull;
-            for (unsigned long long p = p0 + tid; p < ((e + 31) & ~31ull); p += blockDim.x) {
-                const bool in = p >= b && p < e;
-                const uint32_t w = in ? s_stage[p - b] : 0u;
-                const uint32_t an = __reduce_and_sync(0xffffffffu, in ? w : ~0u);
-                const uint32_t orr = __reduce_or_sync(0xffffffffu, w);
-                if (lane == 0) {
-                    atomicAnd(&a.bsum[p >> 5].x, an);
-                    atomicOr(&a.bsum[p >> 5].y, orr);
-                    atomicAnd(&a.ssum[p >> 10].x, an);
-                    atomicOr(&a.ssum[p >> 10].y, orr);
-                }
-            }
-        }
-        if (A > a.capacity - M0) A = (uint32_t)(a.capacity - M0);
-        __threadfence_block();
-        __syncthreads();
+        A = r_append(a, sm, Sc, M0, A, t0, wdef);
         P_TR(3)
     }
-    // clear per-tile state for the next tile
-    for (uint32_t w = tid; w < words; w += blockDim.x) dead[w] = 0;
+    // clear per-tile state for the next tile (a prepared tile's mask was cleared by its preparer)
+    if (!prep)
+        for (uint32_t w = tid; w < words; w += blockDim.x) dead[w] = 0;
     // per-warp reduction, then thread 0 sums the warps' partials (no 64-bit shared atomics,
     // which are emulated with CAS loops)
 #pragma unroll
@@ -1258,43 +1454,123 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         rchk += __shfl_down_sync(0xffffffffu, rchk, o);
         confl += __shfl_down_sync(0xffffffffu, confl, o);
         wdef += __shfl_down_sync(0xffffffffu, wdef, o);
+        pkill += __shfl_down_sync(0xffffffffu, pkill, o);
     }
     const int wid = tid >> 5;
-    if (lane == 0) { s_stat[wid][0] = rchk; s_stat[wid][1] = confl; s_stat[wid][2] = wdef; }
+    if (lane == 0) { r.stat[wid][0] = rchk; r.stat[wid][1] = confl; r.stat[wid][2] = wdef; r.stat[wid][3] = pkill; }
     __syncthreads();
-    if (tid == 0) {
-        for (int w = 0; w < kPWarps; ++w) {
-            pc.resolve_checks += s_stat[w][0];
-            pc.conflicts += s_stat[w][1];
-            pc.w_def += s_stat[w][2];
+    unsigned long long pk = 0;
+    if (wid == 0) {          // warp 0 sums the warps' partials, lane w holding warp w's
+        unsigned long long v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+        if (lane < kPWarps) { v0 = r.stat[lane][0]; v1 = r.stat[lane][1]; v2 = r.stat[lane][2]; v3 = r.stat[lane][3]; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            v0 += __shfl_down_sync(0xffffffffu, v0, o);
+            v1 += __shfl_down_sync(0xffffffffu, v1, o);
+            v2 += __shfl_down_sync(0xffffffffu, v2, o);
+            v3 += __shfl_down_sync(0xffffffffu, v3, o);
         }
+        if (lane == 0) { pc.resolve_checks += v0; pc.conflicts += v1; pc.w_def += v2; pk = v3; }
     }
-    P_TR(4)
     if (tid == 0) {
+        const uint32_t S_true = S - (uint32_t)min(pk, (unsigned long long)S);
         unsigned long long M1 = M0 + A;
         if (M1 > a.capacity) M1 = a.capacity;
         pc.M = M1;
         st->M = M1;
-        if (S) { pc.S_last = S; pc.K_last = K_used; }
+        const uint32_t S_size = a.size_on_screen ? max(S_true, S_screen) : S_true;
+        if (S_size) { pc.S_last = S_size; pc.K_last = K_used; }
         // (tile sizes stay powers of two: a partial tile's length is rounded down first)
-        pc.K_next = p_next_tile(a, 1u << (31 - __clz(K_used)), S, A, t0 + K_used, M1, pc.S_last,
+        pc.K_next = p_next_tile(a, 1u << (31 - __clz(K_used)), S_true, A, t0 + K_used, M1, pc.S_last,
                                 pc.K_last ? pc.K_last : 1u);
         pc.K_used = K_used;
-        pc.S_tile = S;
+        pc.S_tile = S_true;
         pc.A_tile = A;
         st->K_next = pc.K_next;
-        pc.survivors += S;
+        pc.survivors += S_true;
         pc.tiles += 1;
         pc.levels += L;
     }
-    if (a.weight_bound && tid < 33 && s_wmin[tid] != 0xffffffffu && !pc.wfirst[tid] &&
-        M0 + s_wmin[tid] < a.capacity) {
+    P_TR(4)
+#undef P_TR
+    if (a.weight_bound && tid < 33 && r.wmin[tid] != 0xffffffffu && !pc.wfirst[tid] &&
+        M0 + r.wmin[tid] < a.capacity) {
         // first codebook index of each weight (acceptance order is weight-sorted for graded
         // orders); stored +1, 0 = none yet
-        pc.wfirst[tid] = (unsigned int)(M0 + s_wmin[tid] + 1);
+        pc.wfirst[tid] = (unsigned int)(M0 + r.wmin[tid] + 1);
         st->wfirst[tid] = pc.wfirst[tid];
     }
     __syncthreads();
+}
+
+// Prepare a tile for the resolver (pipelined engine; run by a whole CTA while earlier tiles are
+// resolved): gather its survivors, reject those conflicting with the words committed since its
+// screen (codebook[M_s, M_c)), compact the rest in rank order, build their in-tile conflict
+// lists, and store everything in the slot's prep buffer (p_prep_bytes layout).  Survivors beyond
+// one chunk are spilled to `spill` and checked chunk by chunk.  Returns the number stored, or
+// 0xffffffff when more than one chunk is left after the checks (the resolver then does the whole
+// tile itself, from the dead mask, which is left intact); otherwise the dead mask is cleared
+// here.  S_screen: the survivors of the screen.  rchk: work counter.
+__device__ __forceinline__ uint32_t p_prep(const PArgs &a, const PSmem &sm, unsigned long long t0, uint32_t K, int L,
+                                           uint32_t *dead, unsigned long long M_s, unsigned long long M_c,
+                                           uint8_t *buf, uint2 *spill, unsigned long long &rchk, uint32_t &S_screen) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t S = r_gather(a, sm, t0, K, L, dead, spill);
+    S_screen = S;
+    uint32_t *val = reinterpret_cast<uint32_t *>(buf);
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(buf + (size_t)sm.chunk * 4);
+    uint16_t *idx = reinterpret_cast<uint16_t *>(buf + (size_t)sm.chunk * 8);
+    uint4 *adj = reinterpret_cast<uint4 *>(buf + (size_t)sm.chunk * 10);
+    const bool multi = S > sm.chunk;
+    uint32_t out = 0;
+    for (uint32_t c0 = 0; c0 < S; c0 += sm.chunk) {
+        uint32_t Sc = min(sm.chunk, S - c0);
+        if (c0 > 0) {
+            for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                const uint2 e = __ldcg(spill + c0 + j);
+                sm.s_idx[j] = (uint16_t)e.x;
+                sm.s_val[j] = e.y;
+            }
+            __syncthreads();
+        }
+        if (M_c > M_s && Sc > 0) {
+            r_consensus(sm, Sc);
+            r_prior(a, sm, Sc, M_s, M_c, false, rchk);
+            Sc = r_compact(sm, Sc);
+        }
+        if (out + Sc > sm.chunk) return 0xffffffffu;
+        if (multi) {          // collect the compacted chunks in the prep buffer
+            for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                __stcg(val + out + j, sm.s_val[j]);
+                __stcg(idx + out + j, sm.s_idx[j]);
+            }
+            __syncthreads();
+        }
+        out += Sc;
+    }
+    if (multi) {
+        for (uint32_t j = tid; j < out; j += blockDim.x) {
+            sm.s_val[j] = __ldcg(val + j);
+            sm.s_idx[j] = __ldcg(idx + j);
+        }
+        __syncthreads();
+    }
+    const uint32_t S2 = out;
+    if (S2 > 0) {
+        r_consensus(sm, S2);
+        r_units(a, sm, S2, rchk);
+    }
+    for (uint32_t j = tid; j < S2; j += blockDim.x) {
+        __stcg(val + j, sm.s_val[j]);
+        __stcg(cnt + j, sm.s_cnt[j]);
+        __stcg(idx + j, sm.s_idx[j]);
+    }
+    const uint4 *sa = reinterpret_cast<const uint4 *>(sm.s_adj);
+    for (uint32_t q = tid; q < S2 * (kPAdj / 8); q += blockDim.x) __stcg(adj + q, sa[q]);
+    // the mask is not read again: clear it for the next tile that uses the slot
+    for (uint32_t w = tid; w < (K + 31) / 32; w += blockDim.x) dead[w] = 0;
+    __syncthreads();
+    return S2;
 }
 
 // host: the problem / schedule fields of PArgs (gc_persistent.cu)

@@ -3,7 +3,9 @@
 Only plumbing lives here (PyTorch is used for process groups, not for compute):
   share_nccl_id  -- rank 0 creates the NCCL unique id, every rank receives the bytes
   max_over_ranks -- the max of a per-rank number (timing: max over ranks)
-  comm_from_group -- a gc_comm for this rank (world 1: no NCCL)
+  share_peer_handles -- every rank's IPC handles of its tile-exchange buffers, in rank order
+  comm_from_group -- a gc_comm for this rank (world 1: no NCCL); on GPUs it attaches the peers,
+                     so gc_generate_rank runs the pipelined engine with peer stores over NVLink
 The construction itself is gc_generate_rank (libgc.so).
 """
 from __future__ import annotations
@@ -30,6 +32,17 @@ def share_nccl_id(group=None, make_id=None) -> bytes:
     return bytes(t.cpu().numpy().tobytes())
 
 
+def share_peer_handles(group=None, make_handles=None) -> bytes:
+    """All ranks' gc_peer_handles blobs, concatenated in rank order (all-gather of bytes)."""
+    make_handles = make_handles or B.gc_peer_handles
+    dev = _device_for(group)
+    mine = make_handles()
+    t = torch.frombuffer(bytearray(mine), dtype=torch.uint8).to(dev)
+    parts = [torch.zeros_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, t, group=group)
+    return b"".join(bytes(p.cpu().numpy().tobytes()) for p in parts)
+
+
 def max_over_ranks(x: float, group=None) -> float:
     dev = _device_for(group)
     t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
@@ -43,4 +56,7 @@ def comm_from_group(group=None):
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     if world == 1:
         return B.gc_comm_create(None, 0, 1)
-    return B.gc_comm_create(share_nccl_id(group), rank, world)
+    comm = B.gc_comm_create(share_nccl_id(group), rank, world)
+    if dist.get_backend(group) == "nccl" and world <= 8:
+        B.gc_comm_attach_peers(comm, share_peer_handles(group))
+    return comm

@@ -47,8 +47,8 @@ def test_generate_null_pointers_and_bad_options():
     assert B._lib.gc_generate(7, 3, 0, None, None) == 1            # out_count NULL
     assert B._lib.gc_generate(7, 3, 0, None, ctypes.byref(cnt)) == 1   # NULL buffer, capacity 4
     for bad in ({"tile_min": 48}, {"tile_min": 16}, {"tile_max": 1 << 21}, {"tile_min": 1024, "tile_max": 512},
-                {"window0": 1000}, {"emulate_ranks": 3}, {"flags": 0x800}, {"struct_size": 4},
-                {"pipeline_depth": 17}, {"sub_max": 32}, {"partial_s": 16}, {"split_bits": 33}):
+                {"window0": 1000}, {"emulate_ranks": 3}, {"flags": 0x2000}, {"struct_size": 4},
+                {"pipeline_depth": 17}, {"sub_max": 32}, {"partial_s": 16}, {"split_bits": 33}, {"prep_lead": 16}):
         opts = {"struct_size": ctypes.sizeof(B.gc_options)}
         opts.update(bad)
         with pytest.raises(gc.GCError) as e:
@@ -168,3 +168,22 @@ def test_construct_validates_problem():
         with pytest.raises(gc.GCError) as e:
             gc.gc_construct(8, 3, self_orthogonal=True, options={"emulate_ranks": 2}, capacity=64)
         assert e.value.name in ("GC_EUNSUPPORTED", "GC_ECUDA")
+
+
+def test_attach_peers_validation():
+    # argument checks happen before any CUDA call
+    import paper_1507_05398_b200 as gc
+    nb = gc.gc_peer_handle_bytes()
+    assert nb == 128
+    one = gc.gc_comm_create(None, 0, 1)
+    try:
+        with pytest.raises(gc.GCError) as e:
+            gc.gc_comm_attach_peers(one, bytes(nb))
+        assert e.value.name == "GC_EUNSUPPORTED"          # a single rank has no peers
+        with pytest.raises(ValueError):
+            gc.gc_comm_attach_peers(one, bytes(nb + 1))
+    finally:
+        one.close()
+    assert B._lib.gc_comm_attach_peers(None, None, nb) == 1          # GC_EINVAL
+    buf = (ctypes.c_uint8 * 8)()
+    assert B._lib.gc_peer_handles(buf, 8) == 1                       # too small: GC_EINVAL

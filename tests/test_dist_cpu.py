@@ -29,6 +29,10 @@ def _worker(rank, world, port, q):
         out = {}
         ident = gdist.share_nccl_id()
         out["id"] = ident
+        # the peer-handle exchange of the multi-GPU pipelined engine: every rank ends with every
+        # rank's blob, in rank order (fake blobs: IPC handles need a GPU)
+        nb = gc.gc_peer_handle_bytes()
+        out["handles"] = gdist.share_peer_handles(make_handles=lambda: bytes([rank + 1]) * nb)
         out["max"] = gdist.max_over_ranks(10.0 + rank)
         parts = {}
         for K in (1, 7, 32, 33, 64, 256, 4096, 4097, 65536):
@@ -57,6 +61,8 @@ def test_two_rank_host_logic():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res[0]["id"] == res[1]["id"] and len(res[0]["id"]) == 128
+    nb = len(res[0]["handles"]) // world
+    assert res[0]["handles"] == res[1]["handles"] == bytes([1]) * nb + bytes([2]) * nb
     assert res[0]["max"] == res[1]["max"] == 11.0
     for K, (lo0, ln0, kp0) in res[0]["parts"].items():
         lo1, ln1, kp1 = res[1]["parts"][K]

@@ -285,6 +285,14 @@ ENGINE_KNOBS = [
     {"plan_warps": 16},                         # few items per level
     {"geo_head": 64, "split_bits": 1},
     {"flags": 0x400},                           # no shared-memory super-block mirror
+    {"flags": 0x800},                           # no preparing CTAs: the resolver does every tile
+    {"flags": 0x1000},                          # tile sizes from the survivors left after catch-up
+    {"prep_lead": 1, "prep_ctas": 1},
+    {"prep_lead": 6, "prep_ctas": 8, "pipeline_depth": 7},
+    {"prep_ctas": 1, "grid_ctas": 3},           # resolver, one preparing CTA, one screening CTA
+    {"emulate_ranks": 2},                       # multi-rank pipelined engine, emulated on one GPU
+    {"emulate_ranks": 8, "tile_min": 32, "tile_max": 512},   # partitions with no candidates
+    {"emulate_ranks": 4, "pipeline_depth": 2, "prep_lead": 1},
     # tile-barrier engine
     {"flags": TB, "partial_s": 32},             # cut almost every tile after 32 survivors
     {"flags": TB, "partial_s": 4096, "target_accepted": 2048},   # big tiles, multi-chunk resolves
@@ -303,7 +311,7 @@ def test_engine_knobs_invariance(gc, knobs, n, d, o):
 
 def test_pipeline_stats(gc):
     w, st = gpu_code(gc, 20, 3, "lex")
-    assert st["pipeline_depth"] == 4 and st["launches"] == 1
+    assert st["pipeline_depth"] == 8 and st["launches"] == 1 and st["prep_used"] > 0
     assert st["resolve_busy_ms"] > 0 and st["bound_tests"] > 0 and st["checks_exec"] > 0
     w2, st2 = gpu_code(gc, 20, 3, "lex", flags=TB)
     assert np.array_equal(w, w2) and st2["pipeline_depth"] == 0 and st2["bound_tests"] > 0
