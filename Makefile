@@ -22,10 +22,13 @@ $(SRC)/gc_persistent.o: $(SRC)/gc_persistent.cu $(SRC)/gc_screen.cuh $(SRC)/gc_o
 $(SRC)/gc_pipeline.o: $(SRC)/gc_pipeline.cu $(SRC)/gc_screen.cuh $(SRC)/gc_order.cuh $(SRC)/gc_internal.h include/gc.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_pipeline.ptxas.log || (cat $(SRC)/gc_pipeline.ptxas.log; false)
 
+$(SRC)/gc_cw64.o: $(SRC)/gc_cw64.cu $(SRC)/gc_internal.h include/gc.h
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_cw64.ptxas.log || (cat $(SRC)/gc_cw64.ptxas.log; false)
+
 $(SRC)/gc_analysis.o: $(SRC)/gc_analysis.cu $(SRC)/gc_internal.h include/gc.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(SRC)/gc_analysis.ptxas.log || (cat $(SRC)/gc_analysis.ptxas.log; false)
 
-$(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o $(SRC)/gc_persistent.o $(SRC)/gc_pipeline.o $(SRC)/gc_analysis.o
+$(LIB): $(SRC)/gc_engine.o $(SRC)/gc_abi.o $(SRC)/gc_persistent.o $(SRC)/gc_pipeline.o $(SRC)/gc_analysis.o $(SRC)/gc_cw64.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -ldl -lpthread
 
 $(ORACLE): oracle/greedy_oracle.c

@@ -103,13 +103,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows), "samples_under_load": len(sm)}
 
 
-def load_traffic():
-    """dram bytes per screen launch from the committed ncu --set full summary (or None)."""
-    p = os.path.join(ROOT, "profiles", "screen_ncu_summary.json")
+def load_ncu_summary():
+    """Key counters of the dominant kernel from the committed ncu --set full summary of the same
+    workload (profiles/k_pipeline_ncu_summary.json, tools/ncu_summary.py), or {}."""
+    p = os.path.join(ROOT, "profiles", "k_pipeline_ncu_summary.json")
     try:
-        return json.load(open(p)).get("dram_bytes_per_launch")
+        return json.load(open(p))
     except Exception:
-        return None
+        return {}
 
 
 # ------------------------------------------------------------------ CPU oracle
@@ -376,8 +377,10 @@ def run_b200(args):
     if ex and e2e_val is not None:
         e2e_val = stats[-1]["checks_exec"] / (e2e_val * 1e-3)     # e2e_val held ms per step
 
-    # roofline of the dominant kernel (k_screen): executed checks / its summed device time
+    # roofline of the dominant kernel (k_pipeline, the whole construction in one launch): executed
+    # checks / its device time, against the measured rate of the check arithmetic
     checks = sum(s["checks_exec"] for s in stats)
+    tests = sum(s["bound_tests"] for s in stats)
     screen_ms = sum(s["screen_ms"] for s in stats)
     peaks = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz") or 1965.0)
@@ -385,7 +388,9 @@ def run_b200(args):
     per_clk = CHECK_PEAK_PER_CLK_SM.get(d, CHECK_PEAK_PER_CLK_SM["popc"])
     peak = sms * per_clk * sm_max * 1e6
     achieved = checks / (screen_ms * 1e-3) if screen_ms > 0 else 0.0
+    achieved_tests = (checks + tests) / (screen_ms * 1e-3) if screen_ms > 0 else 0.0
     clocks = sampler.summary()
+    ncu = load_ncu_summary()
 
     if rank == 0:
         line = {
@@ -395,26 +400,34 @@ def run_b200(args):
             "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (the whole space F_2^n in the chosen ordering; no dataset)",
             "config": {"workload": args.workload, "M": M, "w_def": w_def,
-                       "parallelism": f"candidate-partitioned x{world}, replicated codebook",
+                       "parallelism": (f"tile screens partitioned over {world} GPUs (peer stores of the mask "
+                                       "words, replicated codebook and resolve)") if world > 1 else "1 GPU",
                        "l2": "flushed between timed steps (512 MiB write)"},
             "w_exec": checks / args.steps,
             "w_exec_per_s": (checks / args.steps) / (ms_per_step * 1e-3),
-            "roofline": {"bound": "alu", "kernel": "k_construct (persistent: screen levels + resolve)",
+            "roofline": {"bound": "alu", "kernel": "k_pipeline (persistent: screen levels, preparation, resolve)",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tchecks/s",
-                         "frac": achieved / peak if peak else None, "traffic": load_traffic(),
+                         "frac": achieved / peak if peak else None,
+                         "traffic": ncu.get("dram_bytes_per_launch") if ncu.get("workload") == args.workload else None,
                          "peak_basis": f"{sms} SM x {per_clk} checks/clk/SM x {sm_max:.0f} MHz (check "
                                        f"arithmetic for d={d} measured by tools/popc_peak.cu, "
                                        "profiles/r01_popc_peak.txt)",
+                         "bound_tests_per_step": tests / args.steps,
+                         "frac_with_bound_tests": achieved_tests / peak if peak else None,
+                         "ncu": {k: ncu.get(k) for k in ("pipes_pct_of_peak_active", "source", "workload")} if ncu else None,
                          "screen_share_of_step": (screen_ms / args.steps) / ms_per_step,
                          "screen_launches_per_step": stats[-1]["screen_launches"],
                          "regime": "latency-bound: the block bound leaves W_exec ~1e-4 of W_def, so a step is "
-                                   "a chain of dependent tiles (levels + grid barriers + in-tile resolve + "
-                                   "commit token); frac is the executed-check rate against the "
-                                   "check-arithmetic peak"},
+                                   "a chain of dependent tile resolves (one resolving CTA), overlapped with the "
+                                   "screen of later tiles and their preparation; frac is the executed-check "
+                                   "rate against the check-arithmetic peak (frac_with_bound_tests also counts "
+                                   "the block-summary tests as one unit each)"},
             "latency": {"tiles_per_step": stats[-1]["tiles"], "levels_per_step": stats[-1]["phases"],
                         "us_per_tile": 1e3 * ms_per_step / max(1, stats[-1]["tiles"]),
-                        "grid_barriers_per_step": stats[-1]["phases"],
-                        "commit_tokens_per_step": stats[-1]["tiles"]},
+                        "resolver_busy_ms": stats[-1]["resolve_busy_ms"],
+                        "resolver_wait_ms": stats[-1]["resolve_wait_ms"],
+                        "tiles_prepared": stats[-1]["prep_used"],
+                        "pipeline_depth": stats[-1]["pipeline_depth"]},
             "e2e": {"value": e2e_val, "unit": "checks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(sum(s["launches"] for s in stats)),
             "clocks": clocks,

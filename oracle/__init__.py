@@ -83,6 +83,9 @@ def lib():
         L.or_greedy_ball_ex.restype = ctypes.c_int64
         L.or_is_self_orthogonal.argtypes = [u32p, ctypes.c_uint64]
         L.or_is_self_orthogonal.restype = ctypes.c_int
+        L.or_greedy_cw64.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint64]
+        L.or_greedy_cw64.restype = ctypes.c_int64
         L.or_orthogonal.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
         L.or_orthogonal.restype = ctypes.c_int
         _lib = L
@@ -285,4 +288,16 @@ def greedy_ball_ex(n, d, ordering="lex", constant_weight=-1, self_orthogonal=Fal
     M = lib().or_greedy_ball_ex(n, d, _p(table), int(constant_weight), int(bool(self_orthogonal)), _p(out), cap)
     if M < 0:
         raise RuntimeError(f"or_greedy_ball_ex -> {M}")
+    return out[:M].copy()
+
+
+def greedy_cw64(n: int, d: int, w: int, ordering="lex", cap: int | None = None) -> np.ndarray:
+    """Constant-weight greedy on 64-bit words, n <= 63: uint64 words in
+    acceptance order.  Orderings: lex / glex (ascending value within the weight class), grlex."""
+    from math import comb
+    cap = comb(n, w) if cap is None else cap
+    out = np.empty(max(cap, 1), dtype=np.uint64)
+    M = lib().or_greedy_cw64(n, d, w, _ord(ordering), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), cap)
+    if M < 0:
+        raise RuntimeError(f"or_greedy_cw64 -> {M}")
     return out[:M].copy()

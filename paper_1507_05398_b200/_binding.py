@@ -262,7 +262,13 @@ def gc_construct(n: int, d: int, ordering="lex", basis=None, constant_weight=-1,
     """Generalised construction (B-ordering basis, constant weight, self-orthogonal) --
     gc_construct().  Returns (codewords uint64 array, stats dict)."""
     prob, keep = _problem(n, d, ordering, basis, constant_weight, self_orthogonal)
-    cap = gc_capacity_bound(n, d) if capacity is None else capacity
+    if capacity is not None:
+        cap = capacity
+    elif n > 32 and constant_weight >= 0:        # 64-bit constant-weight path: at most the weight class
+        from math import comb
+        cap = min(comb(n, constant_weight), 1 << 27)
+    else:
+        cap = gc_capacity_bound(n, d)
     out = np.empty(max(cap, 1), dtype=np.uint64)
     cnt = ctypes.c_uint64(cap)
     st = gc_stats()

@@ -190,8 +190,12 @@ int gc_problem_to_args(const gc_problem *p, RunArgs *a) {
     if (ord < GC_LEX || ord > GC_B_ORDERING) { set_error("unknown ordering"); return GC_EINVAL; }
     if (p->n == 0) { set_error("n must be >= 1"); return GC_EINVAL; }
     if (p->d == 0 || p->d > p->n) { set_error("d must be in [1, n]"); return GC_EINVAL; }
-    if (p->n > 32) { set_error("the GPU path supports n <= 32"); return GC_EUNSUPPORTED; }
     if (p->constant_weight < -1 || p->constant_weight > (int)p->n) { set_error("constant_weight must be -1 or in [0, n]"); return GC_EINVAL; }
+    if (p->n > 63) { set_error("n must be <= 63"); return GC_EUNSUPPORTED; }
+    if (p->n > 32 && (p->constant_weight < 0 || p->self_orthogonal || ord == GC_B_ORDERING || ord == GC_GRAY)) {
+        set_error("n > 32 is supported for constant-weight problems in lex / graded orders only (64-bit words)");
+        return GC_EUNSUPPORTED;
+    }
     if (p->self_orthogonal > 1) { set_error("self_orthogonal must be 0 or 1"); return GC_EINVAL; }
     a->n = p->n; a->d = p->d;
     a->ordering = ord == GC_B_ORDERING ? GC_LEX : ord;
@@ -362,6 +366,7 @@ int gc_construct_device(const gc_problem *problem, const gc_options *opt, uint32
     RunArgs a;
     int rc = gc_problem_to_args(problem, &a);
     if (rc) return rc;
+    if (a.wide()) { set_error("n > 32: 64-bit words, host buffers only (gc_construct)"); return GC_EUNSUPPORTED; }
     rc = resolve_options(opt, &a.opt);
     if (rc) return rc;
     if (!d_codebook || !d_count || capacity == 0) { set_error("d_codebook/d_count NULL or capacity 0"); return GC_EINVAL; }

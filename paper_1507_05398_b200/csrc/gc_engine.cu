@@ -742,6 +742,7 @@ extern "C" int gc_construct(const gc_problem *problem, const gc_options *opt, ui
     if (rc) return rc;
     rc = resolve_options(opt, &a.opt);
     if (rc) return rc;
+    if (a.wide()) return cw64_supported(a) ? cw64_run(a, out_codewords, out_count, stats) : GC_EUNSUPPORTED;
     return host_construct(a, out_codewords, out_count, stats);
 }
 

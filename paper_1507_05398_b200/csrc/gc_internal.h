@@ -80,6 +80,7 @@ struct RunArgs {
     bool self_orthogonal = false;
     int constant_weight = -1;
     bool extended() const { return use_basis || self_orthogonal || constant_weight >= 0; }
+    bool wide() const { return n > 32; }   // 64-bit words: constant-weight problems only (gc_cw64.cu)
 };
 int engine_run(const RunArgs &a);
 int gc_problem_to_args(const gc_problem *p, RunArgs *a);   // gc_abi.cpp (validation, no CUDA)
@@ -91,6 +92,8 @@ bool persistent_supported(const RunArgs &a);   // gc_persistent.cu
 int persistent_run(const RunArgs &a);
 bool persistent_partitioned_supported(const RunArgs &a);
 int persistent_run_partitioned(const RunArgs &a);
+bool cw64_supported(const RunArgs &a);        // gc_cw64.cu (constant weight, n <= 63, host buffers)
+int cw64_run(const RunArgs &a, uint64_t *out_codewords, uint64_t *out_count, gc_stats *stats);
 int engine_ranks_to_vectors_device(int ordering, uint32_t n, uint64_t first, uint64_t count,
                                    uint32_t *d_out, void *stream);
 

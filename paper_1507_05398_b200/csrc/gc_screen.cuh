@@ -1198,17 +1198,21 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
     __syncthreads();
     const uint32_t novf = min(r.novf, kPOvf);
     if (timer) { const unsigned long long t_ = clock64(); timer->r[5] += t_ - tr; tr = t_; }
+    // rounds read the statuses of one buffer and write the next one (the pad bytes after s_status),
+    // so a round never reads a status another thread is writing
+    uint8_t *cur = s_status, *nxt = s_status + sm.chunk;
     int left = 0;
     for (int round = 0; round < 8; ++round) {
         int undecided = 0;
         for (uint32_t j = tid; j < Sc; j += blockDim.x) {
-            if (s_status[j] != 2) continue;
+            const uint8_t sj = cur[j];
+            if (sj != 2) { nxt[j] = sj; continue; }
             const uint32_t cn = s_cnt[j];
             if (cn == kPOvfMark) { undecided = 1; continue; }     // a warp decides it below
             bool acc_nb = false, und_nb = false;
             if (cn <= kPAdj) {
                 for (uint32_t t = 0; t < cn; ++t) {
-                    const uint8_t sk = s_status[s_adj[j * kPAdj + t]];
+                    const uint8_t sk = cur[s_adj[j * kPAdj + t]];
                     acc_nb |= sk == 1;
                     und_nb |= sk == 2;
                 }
@@ -1216,42 +1220,44 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
                 const uint32_t vj = s_val[j];
                 for (uint32_t k = 0; k < j; ++k) {
                     if (p_conflict(a, vj, s_val[k])) {
-                        const uint8_t sk = s_status[k];
+                        const uint8_t sk = cur[k];
                         acc_nb |= sk == 1;
                         und_nb |= sk == 2;
                     }
                 }
             }
-            // a status read in the same round may be stale (2): that only delays
-            if (acc_nb) s_status[j] = 0;
-            else if (!und_nb) s_status[j] = 1;
-            else undecided = 1;
+            const uint8_t ns = acc_nb ? 0 : (!und_nb ? 1 : 2);
+            nxt[j] = ns;
+            undecided |= ns == 2;
         }
         for (uint32_t o = tid >> 5; o < novf; o += blockDim.x >> 5) {
             const uint32_t j = r.ovf[o];
-            if (s_status[j] != 2) continue;                       // warp-uniform
+            if (cur[j] != 2) continue;                            // warp-uniform (copied above)
             const uint32_t vj = s_val[j];
             bool acc_nb = false, und_nb = false;
             for (uint32_t k = lane; k < j; k += 32) {
                 if (p_conflict(a, vj, s_val[k])) {
-                    const uint8_t sk = s_status[k];
+                    const uint8_t sk = cur[k];
                     acc_nb |= sk == 1;
                     und_nb |= sk == 2;
                 }
             }
             acc_nb = __any_sync(0xffffffffu, acc_nb);
             und_nb = __any_sync(0xffffffffu, und_nb);
-            if (lane == 0) {
-                if (acc_nb) s_status[j] = 0;
-                else if (!und_nb) s_status[j] = 1;
-            }
+            if (lane == 0) nxt[j] = acc_nb ? 0 : (!und_nb ? 1 : 2);
+            undecided |= !acc_nb && und_nb;
         }
         if (a.timing && tid == 0) {
             atomicAdd(&st->n_rounds, 1ull);
             atomicMax(&st->n_rounds_max, (unsigned long long)round + 1);
         }
         left = __syncthreads_or(undecided);
+        uint8_t *t = cur; cur = nxt; nxt = t;
         if (!left) break;
+    }
+    if (cur != s_status) {
+        for (uint32_t j = tid; j < Sc; j += blockDim.x) s_status[j] = cur[j];
+        __syncthreads();
     }
     if (timer) { const unsigned long long t_ = clock64(); timer->r[6] += t_ - tr; tr = t_; }
     if (left && tid < 32) {

@@ -113,3 +113,23 @@ def test_extended_problems_need_persistent_engine(gc):
     with pytest.raises(gc.GCError) as e:
         gc.gc_construct(10, 3, self_orthogonal=True, options={"flags": 16})
     assert e.value.name == "GC_EUNSUPPORTED"
+
+
+# ------------- constant weight on 64-bit words, n = 33..35 ("up-to 35")
+
+@pytest.mark.parametrize("ordering", ["lex", "glex", "grlex"])
+@pytest.mark.parametrize("n,d,w", [(33, 4, 4), (35, 4, 4), (35, 6, 5), (33, 2, 3), (35, 8, 4), (34, 6, 6),
+                                   (35, 10, 5), (33, 4, 30)])
+def test_cw64_matches_oracle(gc, ordering, n, d, w):
+    got, st = gc.gc_construct(n, d, ordering=ordering, constant_weight=w)
+    ref = O.greedy_cw64(n, d, w, ordering)
+    assert st["M"] == len(ref)
+    assert np.array_equal(got.astype(np.uint64), ref), (n, d, w, ordering)
+
+
+def test_cw64_unsupported_combinations(gc):
+    for kw in (dict(ordering="gray", constant_weight=4), dict(ordering="lex"),
+               dict(ordering="lex", constant_weight=4, self_orthogonal=True)):
+        with pytest.raises(gc.GCError) as e:
+            gc.gc_construct(34, 4, **kw)
+        assert e.value.name == "GC_EUNSUPPORTED"

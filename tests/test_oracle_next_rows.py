@@ -199,3 +199,55 @@ def test_is_self_orthogonal_positive_small():
     assert O.is_self_orthogonal([])
     assert O.is_self_orthogonal([0])
     assert O.is_self_orthogonal([0, 3, 12, 15])     # [4,2] repetition pairs: 0011, 1100, 1111
+
+
+# ------------------------- constant weight on 64-bit words ("up to 35")
+
+@pytest.mark.parametrize("ordering", ["lex", "glex", "grlex"])
+@pytest.mark.parametrize("n", [33, 35])
+def test_cw64_closed_forms(ordering, n):
+    from math import comb
+    for w in (1, 2, 3):
+        # d = 2: any two distinct weight-w words differ in >= 2 places, so every one is accepted
+        w2 = O.greedy_cw64(n, 2, w, ordering)
+        assert len(w2) == comb(n, w) and len(set(w2.tolist())) == comb(n, w)
+        assert all(bin(int(x)).count("1") == w for x in w2)
+        # d = 2w: supports must be disjoint; the greedy takes consecutive blocks of w coordinates
+        wd = O.greedy_cw64(n, 2 * w, w, ordering)
+        assert len(wd) == n // w
+        acc = 0
+        for x in wd.tolist():
+            assert acc & x == 0
+            acc |= x
+        # d > 2w: no two weight-w words are that far apart
+        if 2 * w + 1 <= n:
+            assert len(O.greedy_cw64(n, 2 * w + 1, w, ordering)) == 1
+    # the orders: ascending / descending values within the class
+    w4 = O.greedy_cw64(n, 2, 4, ordering)
+    assert list(w4) == sorted(w4.tolist(), reverse=(ordering == "grlex"))
+
+
+@pytest.mark.parametrize("ordering", ["lex", "glex", "grlex"])
+@pytest.mark.parametrize("n,d,w", [(12, 4, 5), (14, 4, 4), (16, 6, 6), (18, 4, 3), (20, 6, 5), (13, 3, 6)])
+def test_cw64_matches_u32_oracle(ordering, n, d, w):
+    # the 32-bit constant-weight oracles (pinned in this file) restricted to n <= 32
+    ref = O.greedy_ball_ex(n, d, ordering, constant_weight=w)
+    got = O.greedy_cw64(n, d, w, ordering)
+    assert np.array_equal(got.astype(np.uint32), ref) and got.max(initial=0) < (1 << n)
+
+
+@pytest.mark.parametrize("ordering", ["lex", "grlex"])
+@pytest.mark.parametrize("n", [6, 8, 9])
+def test_cw64_greedy_characterisation(ordering, n):
+    # brute force: in the order of the weight class, a word is in the code iff it is at distance
+    # >= d from every EARLIER code word (Python bit counting, independent of the oracle's code)
+    from itertools import combinations
+    for w in range(1, n):
+        cls = sorted((sum(1 << b for b in c) for c in combinations(range(n), w)), reverse=(ordering == "grlex"))
+        for d in range(1, n + 1):
+            code = O.greedy_cw64(n, d, w, ordering).tolist()
+            pos = {v: i for i, v in enumerate(cls)}
+            for i, v in enumerate(cls):
+                earlier = [c for c in code if pos[c] < i]
+                ok = all(bin(v ^ c).count("1") >= d for c in earlier)
+                assert (v in code) == ok, (n, d, w, v)
