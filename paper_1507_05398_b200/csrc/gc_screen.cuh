@@ -1262,7 +1262,9 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
     if (timer) { const unsigned long long t_ = clock64(); timer->r[6] += t_ - tr; tr = t_; }
     if (left && tid < 32) {
         for (uint32_t j = 0; j < Sc; ++j) {
-            if (s_status[j] != 2) continue;                 // warp-uniform
+            // lane 0 alone reads and writes s_status[j]; the others see it through the shuffle
+            const uint32_t sj = __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)s_status[j] : 0u, 0);
+            if (sj != 2) continue;                          // warp-uniform
             if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
             const uint32_t cn = s_cnt[j];
             bool acc_nb = false;
