@@ -105,7 +105,8 @@ typedef struct gc_options {
     uint32_t prep_lead;      /* pipelined engine: a screening CTA prepares tile i (survivors, their
                                 check against the words committed since its screen, in-tile
                                 conflict lists) once tile i - prep_lead is being resolved; the
-                                resolver then checks only the newer words.  0 = default (2);
+                                resolver then checks only the newer words.  0 = default (1; graded
+                                orders 2);
                                 GC_FLAG_NO_PREP: the resolver does everything                    */
     uint32_t prep_ctas;      /* pipelined engine: CTAs that only prepare tiles (default 2; other
                                 screening CTAs also prepare when idle)                           */

@@ -323,6 +323,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
         PTimers tmr;
         if (a.timing && threadIdx.x == 0) memset(&tmr, 0, sizeof tmr);
         PTimers *timer = (a.timing && threadIdx.x == 0) ? &tmr : nullptr;
+        unsigned long long t_top_p = 0, t_pub_p = 0, t_rp[8] = {0}, t_r0[8];   // diagnostics: prepared tiles
         for (unsigned long long i = 0;; ++i) {
             __syncthreads();
             if (i >= s_issued) break;
@@ -364,14 +365,19 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 }
                 s_mode = mode;
                 const unsigned long long tb = p_now();
+                if (mode) t_top_p += tb - tw;
                 t_wait += tb - tw;
                 t_busy -= tb;
                 tb0 = tb;
             }
             __syncthreads();
             uint32_t *dead = a.qdead + (size_t)si * kQWords;
+            if (timer)
+                for (int k = 0; k < 8; ++k) t_r0[k] = tmr.r[k];
             p_resolve(a, sm, s_t0[si], s_K[si], (int)s_L[si], pc, timer, 0, false, dead, s_Ms[si],
                       s_mode ? &s_pp : nullptr);
+            if (timer && s_mode)
+                for (int k = 0; k < 8; ++k) t_rp[k] += tmr.r[k] - t_r0[k];
             if (threadIdx.x == 0) {
                 const unsigned long long tp = timer ? clock64() : 0;
                 // next descriptor: tile s_issued, screened against the codebook as of now; its
@@ -402,7 +408,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 const unsigned long long te = p_now();
                 t_busy += te;
                 if (s_mode) t_bprep += te - tb0;
-                if (timer) t_pub += clock64() - tp;
+                if (timer) { t_pub += clock64() - tp; if (s_mode) t_pub_p += clock64() - tp; }
             }
         }
         if (threadIdx.x == 0) {
@@ -415,8 +421,13 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
             q->prep_used = n_used;
             q->busy_prep_ns = t_bprep;
             if (timer) {
-                for (int k = 0; k < 8; ++k) st->t_r[k] = tmr.r[k];
+                for (int k = 0; k < 8; ++k) {
+                    st->t_r[k] = tmr.r[k];
+                    st->t_level[k] = t_rp[k];
+                }
                 st->t_sync = t_pub;
+                st->t_level[8] = t_pub_p;
+                st->t_level[9] = t_top_p;
             }
         }
     } else {
@@ -778,7 +789,11 @@ int pipeline_run(const RunArgs &r) {
     // previous tile is committed everywhere when 2 x depth < the ring
     if (world > 1) a.depth = std::min(a.depth, kQRing / 2 - 1);
     a.chunk = kQChunk;
-    a.prep_lead = (r.opt.flags & GC_FLAG_NO_PREP) ? 0 : (int)(r.opt.prep_lead ? r.opt.prep_lead : 2u);
+    // preparation lead: 1 tile for lex / Gray / B-orders (the resolver then checks only the last
+    // tile's words), 2 for graded orders, whose screens are the binding stage and whose preparers
+    // need the slack (tools/r02g.sh sweep, profiles/r02g_knob_sweep.log)
+    const bool graded = (r.ordering == GRADED_LEX || r.ordering == GRADED_REVLEX) && !r.use_basis;
+    a.prep_lead = (r.opt.flags & GC_FLAG_NO_PREP) ? 0 : (int)(r.opt.prep_lead ? r.opt.prep_lead : graded ? 2u : 1u);
     a.size_on_screen = (r.opt.flags & GC_FLAG_SIZE_ON_TRUE) ? 0 : 1;
     a.world = world;
     a.rank = r.world > 1 ? r.rank : 0;
@@ -891,6 +906,11 @@ int pipeline_run(const RunArgs &r) {
                     "append %.2f clear+stats %.2f publish %.2f us (SM cycles at 1965 MHz)\n", f.t_r[0] / T / c,
                     f.t_r[1] / T / c, f.t_r[5] / T / c, f.t_r[6] / T / c, f.t_r[2] / T / c, f.t_r[3] / T / c,
                     f.t_r[4] / T / c, f.t_sync / T / c);
+            const double P = (double)std::max(1ull, hq.prep_used);
+            fprintf(stderr, "[gc]   prepared tiles: CAS+reset %.2f (ns clock) load %.2f consensus+prior %.2f status %.2f "
+                    "rounds %.2f sequential %.2f append %.2f stats %.2f publish %.2f us\n", f.t_level[9] / P / 1e3,
+                    f.t_level[0] / P / c, f.t_level[1] / P / c, f.t_level[5] / P / c, f.t_level[6] / P / c,
+                    f.t_level[2] / P / c, f.t_level[3] / P / c, f.t_level[4] / P / c, f.t_level[8] / P / c);
             fprintf(stderr, "[gc]   per tile: survivors %.1f, accepted %.1f, resolve checks %.0f, levels %.2f; "
                     "largest S %llu, %llu multi-chunk tiles, %.2f rounds, %.2f sequential\n", f.survivors / T, f.M / T,
                     f.resolve_checks / T, f.levels / T, f.s_max, f.n_chunked, f.n_rounds / T, f.n_seq / T);
