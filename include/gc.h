@@ -110,6 +110,8 @@ typedef struct gc_options {
                                 GC_FLAG_NO_PREP: the resolver does everything                    */
     uint32_t prep_ctas;      /* pipelined engine: CTAs that only prepare tiles (default 2; other
                                 screening CTAs also prepare when idle)                           */
+    uint32_t burst_chunk;    /* survivors decided per sub-chunk when a tile has more than one resolve
+                                chunk of them (>= 32, default 512)                               */
 } gc_options;
 
 #define GC_FLAG_NO_EARLY_EXIT  0x1u  /* screen every candidate against the whole codebook, one phase     */

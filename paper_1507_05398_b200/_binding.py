@@ -45,7 +45,7 @@ class gc_options(ctypes.Structure):
                 ("target_accepted", ctypes.c_uint32), ("items_per_warp", ctypes.c_uint32),
                 ("sub_max", ctypes.c_uint32), ("geo_head", ctypes.c_uint32), ("split_bits", ctypes.c_uint32),
                 ("partial_s", ctypes.c_uint32), ("grid_ctas", ctypes.c_uint32), ("plan_warps", ctypes.c_uint32),
-                ("prep_lead", ctypes.c_uint32), ("prep_ctas", ctypes.c_uint32)]
+                ("prep_lead", ctypes.c_uint32), ("prep_ctas", ctypes.c_uint32), ("burst_chunk", ctypes.c_uint32)]
 
 
 GC_B_ORDERING = 4

@@ -43,11 +43,12 @@ int resolve_options(const gc_options *opt, Options *out) {
         o.plan_warps = opt->plan_warps;
         o.prep_lead = opt->prep_lead;
         o.prep_ctas = opt->prep_ctas;
+        o.burst_chunk = opt->burst_chunk;
     }
     if (o.pipeline_depth > 16 || (o.sub_max && o.sub_max < 64) || (o.partial_s && o.partial_s < 32) ||
-        o.split_bits > 32 || o.prep_lead > 15 || o.prep_ctas > 64) {
+        o.split_bits > 32 || o.prep_lead > 15 || o.prep_ctas > 64 || (o.burst_chunk && o.burst_chunk < 32)) {
         set_error("pipeline_depth must be <= 16, sub_max >= 64, partial_s >= 32, split_bits <= 32, prep_lead <= 15, "
-                  "prep_ctas <= 64");
+                  "prep_ctas <= 64, burst_chunk >= 32");
         return GC_EINVAL;
     }
     if (o.growth > 12) {          // 0 = engine default

@@ -27,7 +27,7 @@ struct Options {
     // persistent engines (0 = default; gc.h gc_options)
     uint32_t pipeline_depth = 0, target_accepted = 0, items_per_warp = 0, sub_max = 0, geo_head = 0,
              split_bits = 0, partial_s = 0, grid_ctas = 0, plan_warps = 0, prep_lead = 0,
-             prep_ctas = 0;
+             prep_ctas = 0, burst_chunk = 0;
     bool geo_head_set = false;
 };
 int resolve_options(const gc_options *opt, Options *out);   // GC_OK / GC_EINVAL

@@ -443,6 +443,7 @@ void p_fill_args(const RunArgs &r, PArgs *pa) {
     a.split_bits = o.split_bits ? (int)o.split_bits : lex_single ? kPSplitBits - 2 : kPSplitBits;
     a.geo_head = o.geo_head ? o.geo_head : 8192u;
     a.partial_s = o.partial_s ? o.partial_s : graded ? 1024u : 512u;
+    a.burst_chunk = o.burst_chunk ? o.burst_chunk : 512u;
     a.target_accepted = o.target_accepted ? o.target_accepted
                         : r.use_basis ? kPTargetAccepted
                         : r.ordering >= GRADED_LEX ? 4 * kPTargetAccepted

@@ -176,9 +176,11 @@ __device__ __forceinline__ void q_flag_empty(const PArgs &a, int si, unsigned lo
 // CTAs that validated one of its levels may still be about to claim items from it (a claim is an
 // add), so the counters are reset only once none is inside.  Done ahead of time (while waiting
 // for a screen) when the ring is deeper than the pipeline.
-__device__ __forceinline__ void q_reset(QCtl *q, unsigned long long i) {
+__device__ __forceinline__ void q_reset(QCtl *q, unsigned long long i, unsigned int inside_seen = 1u) {
     QSlot &sl = q->slot[i % kQRing];
-    while (q_ld_acquire32(&sl.inside) != 0) __nanosleep(32);
+    // `inside` of a committed tile's slot only decreases: a 0 read earlier (acquire) stays valid
+    if (inside_seen != 0)
+        while (q_ld_acquire32(&sl.inside) != 0) __nanosleep(32);
     const unsigned long long tag = (i + 1) & 0xffffffffull;
     for (int l = 0; l < kPMaxLevels; ++l) { sl.claim[l] = tag << 32; sl.done[l] = 0; }
 }
@@ -320,6 +322,8 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
             }
         }
         unsigned long long t_wait = 0, t_busy = 0, t_pub = 0, n_used = 0, t_bprep = 0, tb0 = 0;
+        unsigned long long w_ahead = 0;    // thread 0: the next tile's prep word, read ahead
+        unsigned int in_ahead = 1u;        // thread 0: `inside` of the slot the next tile resets, read ahead
         PTimers tmr;
         if (a.timing && threadIdx.x == 0) memset(&tmr, 0, sizeof tmr);
         PTimers *timer = (a.timing && threadIdx.x == 0) ? &tmr : nullptr;
@@ -331,14 +335,18 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
             QSlot *sl = &q->slot[si];
             if (threadIdx.x == 0) {
                 const unsigned long long tw = p_now();
-                if (pre_reset && s_next < a.t_end) q_reset(q, i + a.depth);
+                if (pre_reset && s_next < a.t_end) q_reset(q, i + a.depth, i ? in_ahead : 1u);
                 // Prepared by another CTA?  One CAS: it either hands over the finished preparation
                 // or takes the tile over (nobody started on it: this CTA does all of it).
                 int mode = 0;
                 bool need_phase = true;
                 if (a.prep_lead > 0) {
                     const unsigned long long open = q_pw(i, kPrepOpen, 0, 0);
-                    unsigned long long w = q_cas_acqrel(&sl->prep, open, q_pw(i, kPrepResolver, 0, 0));
+                    // the word read (acquire) while the previous commit was being published: a
+                    // finished preparation is final, anything else needs the CAS
+                    unsigned long long w = w_ahead;
+                    if (!(w >> 52 == ((i + 1) & 0xfffull) && q_pw_state(w) == kPrepDone))
+                        w = q_cas_acqrel(&sl->prep, open, q_pw(i, kPrepResolver, 0, 0));
                     if (w != open) {
                         while (q_pw_state(w) != kPrepDone) { __nanosleep(32); w = q_ld_acquire(&sl->prep); }
                         need_phase = false;               // prepared implies screened
@@ -396,6 +404,9 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                     s_next += Kn;
                     ++s_issued;
                 }
+                // look at the next tile's preparation now: the load's round trip overlaps the fence
+                if (a.prep_lead > 0 && i + 1 < s_issued) w_ahead = q_ld_acquire(&q->slot[(i + 1) % kQRing].prep);
+                if (pre_reset) in_ahead = q_ld_acquire32(&q->slot[(i + 1 + a.depth) % kQRing].inside);
                 // one fence releases the tile's appended words and summaries (the whole CTA's,
                 // ordered by the barrier at the end of p_resolve) and the new descriptor
                 __threadfence();

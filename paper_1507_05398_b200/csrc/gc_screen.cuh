@@ -136,6 +136,7 @@ struct PArgs {
     uint2 *qspill;                     // per ring slot: kPMaxTile (the preparer's survivors beyond one chunk)
     int prep_lead;                     // tile i is prepared once tile i - prep_lead is being resolved (0: never)
     int prep_ctas;                     // CTAs 1 .. prep_ctas only prepare tiles (never screen)
+    uint32_t burst_chunk;              // survivors decided per sub-chunk of a tile with more than one chunk
     int size_on_screen;                // tile sizes bound the survivors of the (older-codebook) screen, which
                                        // the resolve handles, not only those left after the catch-up checks
     // multi-rank pipelined engine: the screen of every tile is split over `world` ranks (whole mask
@@ -1201,7 +1202,7 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
     // rounds read the statuses of one buffer and write the next one (the pad bytes after s_status),
     // so a round never reads a status another thread is writing
     uint8_t *cur = s_status, *nxt = s_status + sm.chunk;
-    int left = 0;
+    int left = 0, prev_cnt = 1 << 30;
     for (int round = 0; round < 8; ++round) {
         int undecided = 0;
         for (uint32_t j = tid; j < Sc; j += blockDim.x) {
@@ -1251,9 +1252,14 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
             atomicAdd(&st->n_rounds, 1ull);
             atomicMax(&st->n_rounds_max, (unsigned long long)round + 1);
         }
-        left = __syncthreads_or(undecided);
+        // threads still holding an undecided survivor; rounds that settle less than a quarter of
+        // them (long chains of conflicts, e.g. a tile just past a high-bit boundary) hand over to
+        // the group-sequential tail below
+        const int cnt = __syncthreads_count(undecided);
         uint8_t *t = cur; cur = nxt; nxt = t;
-        if (!left) break;
+        left = cnt;
+        if (!cnt || (round >= 1 && cnt * 4 > prev_cnt * 3)) break;
+        prev_cnt = cnt;
     }
     if (cur != s_status) {
         for (uint32_t j = tid; j < Sc; j += blockDim.x) s_status[j] = cur[j];
@@ -1261,22 +1267,49 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
     }
     if (timer) { const unsigned long long t_ = clock64(); timer->r[6] += t_ - tr; tr = t_; }
     if (left && tid < 32) {
-        for (uint32_t j = 0; j < Sc; ++j) {
-            // lane 0 alone reads and writes s_status[j]; the others see it through the shuffle
-            const uint32_t sj = __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)s_status[j] : 0u, 0);
-            if (sj != 2) continue;                          // warp-uniform
-            if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
-            const uint32_t cn = s_cnt[j];
-            bool acc_nb = false;
-            if (cn <= kPAdj) {
-                if (lane < cn) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
-            } else {
-                const uint32_t vj = s_val[j];
-                for (uint32_t k = lane; k < j; k += 32)
-                    acc_nb |= (s_status[k] == 1) && p_conflict(a, vj, s_val[k]);
+        // warp 0 finishes the undecided survivors group by group (32 consecutive ones, in rank
+        // order): lane t owns survivor g0 + t.  A member is rejected by an accepted survivor
+        // before the group (its conflict list, or a scan for an overflow node), else decided by
+        // the group's own greedy over a 32 x 32 conflict bit matrix held in registers.
+        for (uint32_t g0 = 0; g0 < Sc; g0 += 32) {
+            const uint32_t j = g0 + lane;
+            const bool in = j < Sc;
+            const uint32_t sj = in ? (uint32_t)s_status[j] : 0u;   // lane-owned until the write below
+            const unsigned und = __ballot_sync(0xffffffffu, in && sj == 2);
+            if (!und) continue;
+            if (a.timing && lane == 0) atomicAdd(&st->n_seq, (unsigned long long)__popc(und));
+            const uint32_t vj = in ? s_val[j] : 0u;
+            const uint32_t cn = in ? s_cnt[j] : 0u;
+            bool pre = false;
+            if (sj == 2 && cn <= kPAdj)
+                for (uint32_t t = 0; t < cn; ++t) {
+                    const uint32_t k = s_adj[j * kPAdj + t];
+                    pre |= k < g0 && s_status[k] == 1;
+                }
+            unsigned ovm = __ballot_sync(0xffffffffu, sj == 2 && cn > kPAdj);
+            while (ovm) {                                  // overflow nodes: the warp scans for them
+                const int t = __ffs(ovm) - 1;
+                ovm &= ovm - 1;
+                const uint32_t vt = __shfl_sync(0xffffffffu, vj, t);
+                bool c = false;
+                for (uint32_t k = lane; k < g0; k += 32) c |= s_status[k] == 1 && p_conflict(a, vt, s_val[k]);
+                c = __any_sync(0xffffffffu, c);
+                if (lane == t) pre |= c;
             }
-            acc_nb = __any_sync(0xffffffffu, acc_nb);
-            if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
+            uint32_t inmask = 0;                           // earlier members of the group in conflict
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                const uint32_t vt = __shfl_sync(0xffffffffu, vj, t);
+                if (t < lane && p_conflict(a, vj, vt)) inmask |= 1u << t;
+            }
+            const unsigned prem = __ballot_sync(0xffffffffu, pre);
+            unsigned acc = __ballot_sync(0xffffffffu, in && sj == 1);
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                const uint32_t im = __shfl_sync(0xffffffffu, inmask, t);
+                if (((und & ~prem) >> t & 1u) && !(im & acc)) acc |= 1u << t;
+            }
+            if (sj == 2) s_status[j] = (acc >> lane & 1u) ? 1 : 0;
             __syncwarp();
         }
     }
@@ -1409,9 +1442,19 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
     unsigned long long rchk = 0, confl = 0, wdef = 0, pkill = 0;
     const unsigned long long M0 = pc.M;
     uint32_t A = 0;                   // accepted so far in this tile (codebook[M0, M0+A))
-    for (uint32_t c0 = 0; c0 < S; c0 += kPChunk) {
-        uint32_t Sc = min(kPChunk, S - c0);
-        if (c0 > 0) {
+    // More survivors than one chunk (a "burst": e.g. a tile just past a high-bit boundary, where
+    // most candidates survive a screen against an older codebook and kill each other): decided in
+    // sub-chunks of burst_chunk from a.surv -- each one checked against the words accepted in the
+    // earlier ones first, so the in-chunk conflict lists (quadratic) stay small.
+    const bool multi = S > kPChunk;
+    const uint32_t step = multi ? min(kPChunk, max(32u, a.burst_chunk)) : kPChunk;
+    if (multi) {
+        for (uint32_t j = tid; j < kPChunk; j += blockDim.x) a.surv[j] = make_uint2(sm.s_idx[j], sm.s_val[j]);
+        __syncthreads();
+    }
+    for (uint32_t c0 = 0; c0 < S; c0 += step) {
+        uint32_t Sc = min(step, S - c0);
+        if (multi) {
             for (uint32_t j = tid; j < Sc; j += blockDim.x) {
                 const uint2 e = __ldcg(a.surv + c0 + j);
                 sm.s_idx[j] = (uint16_t)e.x;

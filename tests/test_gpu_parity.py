@@ -279,6 +279,7 @@ ENGINE_KNOBS = [
     {"pipeline_depth": 2},
     {"pipeline_depth": 16, "tile_min": 32, "tile_max": 256},   # deep, tiny tiles: long prior ranges
     {"pipeline_depth": 8, "target_accepted": 4096},            # big tiles: multi-chunk resolves
+    {"target_accepted": 4096, "burst_chunk": 32, "flags": 0x800},   # tiny sub-chunks of bursts
     {"grid_ctas": 2},                           # one resolving CTA, one screening CTA
     {"grid_ctas": 3, "items_per_warp": 8},
     {"sub_max": 64},                            # many tiny items
