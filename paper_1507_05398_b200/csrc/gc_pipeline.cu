@@ -37,6 +37,9 @@ constexpr int kQRing = kQRingMax;   // tile slots; the pipeline depth D <= kQRin
 constexpr uint32_t kQChunk = 2048;  // survivors per resolve chunk (and per prepared tile)
 constexpr uint32_t kQWords = kPMaxTile / 32;
 constexpr unsigned long long kQM = (1ull << 40) - 1;   // QCtl::cm: committed tiles << 40 | M
+// watchdog: the resolver gives up (st->error = 2) when one tile's screen, preparation or peer flags
+// have not arrived after this long (a healthy tile takes microseconds to milliseconds)
+constexpr unsigned long long kQStallNs = 30ull * 1000 * 1000 * 1000;
 
 // QSlot::prep packs everything the resolver needs from a preparation into one word, so that
 // its CAS (or the poll that sees it finished) is the only round trip:
@@ -328,9 +331,11 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
         if (a.timing && threadIdx.x == 0) memset(&tmr, 0, sizeof tmr);
         PTimers *timer = (a.timing && threadIdx.x == 0) ? &tmr : nullptr;
         unsigned long long t_top_p = 0, t_pub_p = 0, t_rp[8] = {0}, t_r0[8];   // diagnostics: prepared tiles
+        __shared__ int s_stall;
+        if (threadIdx.x == 0) s_stall = 0;
         for (unsigned long long i = 0;; ++i) {
             __syncthreads();
-            if (i >= s_issued) break;
+            if (i >= s_issued || s_stall) break;
             const int si = (int)(i % kQRing);
             QSlot *sl = &q->slot[si];
             if (threadIdx.x == 0) {
@@ -348,7 +353,11 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                     if (!(w >> 52 == ((i + 1) & 0xfffull) && q_pw_state(w) == kPrepDone))
                         w = q_cas_acqrel(&sl->prep, open, q_pw(i, kPrepResolver, 0, 0));
                     if (w != open) {
-                        while (q_pw_state(w) != kPrepDone) { __nanosleep(32); w = q_ld_acquire(&sl->prep); }
+                        while (q_pw_state(w) != kPrepDone) {
+                            __nanosleep(32);
+                            w = q_ld_acquire(&sl->prep);
+                            if (p_now() - tw > kQStallNs) { s_stall = 1; break; }
+                        }
                         need_phase = false;               // prepared implies screened
                         if (q_pw_S(w) != kPrepTooMany) {
                             const uint8_t *buf = a.qprep + (size_t)si * p_prep_bytes(kPChunk);
@@ -369,6 +378,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                         const unsigned long long ph = q_ld_acquire(&sl->phase);
                         if ((ph >> 8) == i + 1 && (uint32_t)(ph & 0xff) >= s_L[si] && q_peers_in(a, si, i)) break;
                         __nanosleep(32);
+                        if (p_now() - tw > kQStallNs) { s_stall = 1; break; }
                     }
                 }
                 s_mode = mode;
@@ -379,6 +389,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 tb0 = tb;
             }
             __syncthreads();
+            if (s_stall) break;          // watchdog: a screen, a preparation or a peer never arrived
             uint32_t *dead = a.qdead + (size_t)si * kQWords;
             if (timer)
                 for (int k = 0; k < 8; ++k) t_r0[k] = tmr.r[k];
@@ -423,6 +434,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
             }
         }
         if (threadIdx.x == 0) {
+            if (s_stall) st->error = 2;
             q_st_release32(&q->finished, 1u);
             pc.resolve_checks += __ldcg(&q->prep_rchk);   // every preparation was consumed (acquired)
             p_count_store(pc, st);
@@ -926,6 +938,7 @@ int pipeline_run(const RunArgs &r) {
                     "largest S %llu, %llu multi-chunk tiles, %.2f rounds, %.2f sequential\n", f.survivors / T, f.M / T,
                     f.resolve_checks / T, f.levels / T, f.s_max, f.n_chunked, f.n_rounds / T, f.n_seq / T);
         }
+        if (h.error == 2) { set_error("pipelined engine stalled: a screen, preparation or peer never arrived"); return GC_EINTERNAL; }
         if (h.error) { set_error("codebook capacity exceeded"); return GC_ENOSPC; }
     }
     return GC_OK;

@@ -1252,13 +1252,13 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
             atomicAdd(&st->n_rounds, 1ull);
             atomicMax(&st->n_rounds_max, (unsigned long long)round + 1);
         }
-        // threads still holding an undecided survivor; rounds that settle less than a quarter of
-        // them (long chains of conflicts, e.g. a tile just past a high-bit boundary) hand over to
-        // the group-sequential tail below
+        // threads still holding an undecided survivor; when many are left and a round settles less
+        // than a quarter of them (long chains of conflicts, e.g. a tile just past a high-bit
+        // boundary) the group-sequential tail below takes over
         const int cnt = __syncthreads_count(undecided);
         uint8_t *t = cur; cur = nxt; nxt = t;
         left = cnt;
-        if (!cnt || (round >= 1 && cnt * 4 > prev_cnt * 3)) break;
+        if (!cnt || (round >= 1 && cnt > 96 && cnt * 4 > prev_cnt * 3)) break;
         prev_cnt = cnt;
     }
     if (cur != s_status) {

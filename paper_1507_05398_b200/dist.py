@@ -10,6 +10,8 @@ The construction itself is gc_generate_rank (libgc.so).
 """
 from __future__ import annotations
 
+import warnings
+
 import torch
 import torch.distributed as dist
 
@@ -58,5 +60,17 @@ def comm_from_group(group=None):
         return B.gc_comm_create(None, 0, 1)
     comm = B.gc_comm_create(share_nccl_id(group), rank, world)
     if dist.get_backend(group) == "nccl" and world <= 8:
-        B.gc_comm_attach_peers(comm, share_peer_handles(group))
+        handles = share_peer_handles(group)
+        ok = True
+        try:
+            B.gc_comm_attach_peers(comm, handles)
+        except B.GCError as e:                      # no peer access: the tile-barrier NCCL path
+            ok = False
+            warnings.warn(f"gc_comm_attach_peers failed ({e}); using the NCCL all-gather engine")
+        # every rank must take the same engine
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=_device_for(group))
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if not int(flag.item()) and ok:
+            comm.close()
+            comm = B.gc_comm_create(share_nccl_id(group), rank, world)
     return comm
