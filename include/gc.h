@@ -138,6 +138,10 @@ typedef struct gc_options {
 #define GC_FLAG_SIZE_ON_TRUE   0x1000u /* pipelined engine: size tiles on the survivors left after the
                                         checks against the newest words (default: on the survivors of
                                         the screen against the older codebook, which the resolve gets) */
+#define GC_FLAG_NO_PARITY_BOUND 0x2000u /* block bound without the weight-parity refinement (n <= 30:
+                                        when a block's codewords and a warp's candidates each have one
+                                        weight parity, the bound rounds up to the parity of every
+                                        distance)                                                    */
 #define GC_FLAG_KERNEL_TIMING  0x8u  /* bracket every screen launch with CUDA events on the launching
                                         stream; fills gc_stats.screen_ms (benchmarking)               */
 

@@ -30,6 +30,7 @@ GC_FLAG_NO_BLOCK_BOUND = 0x80
 GC_FLAG_TILE_BARRIERS = 0x100
 GC_FLAG_NO_PREP = 0x800
 GC_FLAG_SIZE_ON_TRUE = 0x1000
+GC_FLAG_NO_PARITY_BOUND = 0x2000
 GC_FLAG_DEBUG_PHASES = 0x200
 GC_FLAG_NO_SUP_SMEM = 0x400
 

@@ -444,6 +444,7 @@ void p_fill_args(const RunArgs &r, PArgs *pa) {
     a.geo_head = o.geo_head ? o.geo_head : 8192u;
     a.partial_s = o.partial_s ? o.partial_s : graded ? 1024u : 512u;
     a.burst_chunk = o.burst_chunk ? o.burst_chunk : 512u;
+    a.par = (a.bound && r.n <= 30 && !(o.flags & GC_FLAG_NO_PARITY_BOUND)) ? 1 : 0;
     a.target_accepted = o.target_accepted ? o.target_accepted
                         : r.use_basis ? kPTargetAccepted
                         : r.ordering >= GRADED_LEX ? 4 * kPTargetAccepted

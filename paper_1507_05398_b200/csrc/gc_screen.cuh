@@ -137,6 +137,7 @@ struct PArgs {
     int prep_lead;                     // tile i is prepared once tile i - prep_lead is being resolved (0: never)
     int prep_ctas;                     // CTAs 1 .. prep_ctas only prepare tiles (never screen)
     uint32_t burst_chunk;              // survivors decided per sub-chunk of a tile with more than one chunk
+    int par;                           // block-bound summaries carry the weight parity in bit 31 (n <= 30)
     int size_on_screen;                // tile sizes bound the survivors of the (older-codebook) screen, which
                                        // the resolve handles, not only those left after the catch-up checks
     // multi-rank pipelined engine: the screen of every tile is split over `world` ranks (whole mask
@@ -272,6 +273,26 @@ __device__ __forceinline__ uint32_t p_lb(uint32_t bA, uint32_t bO, uint32_t cA, 
     return (uint32_t)__popc(((bA & ~cO) | (cA & ~bO)) & nmask);
 }
 
+// The same bound on the screen's parity-tagged summaries (a.par, n <= 30: bit 31 of every word
+// that enters an AND / OR is the parity of its weight).  dist(v, c) = wt(v) + wt(c) mod 2, so when
+// every codeword of the block and every candidate of the warp have one weight parity each (AND
+// and OR agree in bit 31 on both sides), every distance has the parity of their sum and the
+// bound rounds up to it (graded orders: a block inside one weight class, d = 4: a bound of 3
+// between equal parities proves >= 4).
+__device__ __forceinline__ uint32_t p_lbs(const PArgs &a, uint32_t bA, uint32_t bO, uint32_t cA, uint32_t cO) {
+    uint32_t lb = (uint32_t)__popc(((bA & ~cO) | (cA & ~bO)) & a.nmask);
+    if (a.par) {
+        const uint32_t uniform = ~((bA ^ bO) | (cA ^ cO)) >> 31;
+        lb += uniform & ((lb ^ ((bO ^ cO) >> 31)) & 1u);
+    }
+    return lb;
+}
+
+// a word with its weight parity in bit 31 (parity-tagged summaries, a.par)
+__device__ __forceinline__ uint32_t p_ptag(const PArgs &a, uint32_t v) {
+    return a.par ? (v | ((uint32_t)__popc(v) << 31)) : v;
+}
+
 // checks of the lane's R candidates against the (nv <= 32) codewords held by lanes 0..nv-1
 template <int R, int MIX>
 __device__ __forceinline__ void p_block(uint32_t cur, int nv, const uint32_t (&v)[R], uint32_t (&m)[R]) {
@@ -357,7 +378,7 @@ __device__ __forceinline__ bool p_scan_blocks(const PArgs &a, long long r_lo, lo
         bool pass = false;
         if (k >= kb) {
             const uint2 bs = __ldcg(a.bsum + k);
-            pass = p_lb(bs.x, bs.y, cA, cO, a.nmask) < a.d;
+            pass = p_lbs(a, bs.x, bs.y, cA, cO) < a.d;
             ++tests;
         }
         const uint32_t mask = __ballot_sync(0xffffffffu, pass);
@@ -447,7 +468,7 @@ __device__ __forceinline__ uint32_t p_scan_window(const PArgs &a, const uint32_t
         bool pass = false;
         if (k >= kb) {
             const uint2 bs = wsum[k - k0];
-            pass = p_lb(bs.x, bs.y, cA, cO, a.nmask) < a.d;
+            pass = p_lbs(a, bs.x, bs.y, cA, cO) < a.d;
             ++tests;
         }
         uint32_t mask = __ballot_sync(0xffffffffu, pass);
@@ -489,7 +510,7 @@ __device__ __forceinline__ uint32_t p_scan_bound(const PArgs &a, long long lo, l
         bool pass = false;
         if (sb >= sb_lo) {
             const uint2 ss = sb < (long long)a.nsup_smem ? s_sup[sb] : __ldcg(a.ssum + sb);
-            pass = p_lb(ss.x, ss.y, cA, cO, a.nmask) < a.d;
+            pass = p_lbs(a, ss.x, ss.y, cA, cO) < a.d;
             ++tests;
         }
         uint32_t smask = __ballot_sync(0xffffffffu, pass);
@@ -508,7 +529,7 @@ __device__ __forceinline__ uint32_t p_scan_bound(const PArgs &a, long long lo, l
                 bool bp = false;
                 if (k >= kb && k <= kt) {
                     const uint32_t *e = sstage + sl * 64 + 2 * (31 - lane);
-                    bp = p_lb(e[0], e[1], cA, cO, a.nmask) < a.d;
+                    bp = p_lbs(a, e[0], e[1], cA, cO) < a.d;
                     ++tests;
                 }
                 const uint32_t bm = __ballot_sync(0xffffffffu, bp);
@@ -675,7 +696,7 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                 uint32_t la = ~0u, lo_ = 0u;
 #pragma unroll
                 for (int r = 0; r < R; ++r)
-                    if (live[r]) { la &= v[r]; lo_ |= v[r]; }
+                    if (live[r]) { const uint32_t vt = p_ptag(a, v[r]); la &= vt; lo_ |= vt; }
                 const uint32_t cA = __reduce_and_sync(0xffffffffu, la), cO = __reduce_or_sync(0xffffffffu, lo_);
                 uint32_t *stg = lv.stage + (threadIdx.x >> 5) * kPWarpStage;
                 uint32_t tests = 0;
@@ -683,7 +704,7 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                     return lv.win ? p_scan_window<R, MIX>(a, lv.win, lv.wsum, lv.win_lo, s_lo, s_hi, sA, sO, v, mm, tests)
                                   : p_scan_bound<R, MIX>(a, s_lo, s_hi, sA, sO, v, mm, stg, lv.s_sup, tests);
                 };
-                const uint32_t vary = cO & ~cA;            // bits on which the live candidates differ
+                const uint32_t vary = cO & ~cA & a.nmask;  // bits on which the live candidates differ
                 // (not for graded orders: a weight class in colex order varies many bits by
                 // nature, and the weight bound already cuts their windows)
                 if (__popc(vary) <= a.split_bits || (a.ord >= GRADED_LEX && !a.use_basis)) {
@@ -702,7 +723,7 @@ __device__ __forceinline__ void p_item(const PArgs &a, const PLevel &lv, unsigne
                         for (int r = 0; r < R; ++r) {
                             const bool in = live[r] && (((v[r] & hb) != 0) == (half == 1));
                             mm[r] = in ? m[r] : 0u;
-                            if (in) { ha &= v[r]; ho |= v[r]; any_h = true; }
+                            if (in) { const uint32_t vt = p_ptag(a, v[r]); ha &= vt; ho |= vt; any_h = true; }
                         }
                         if (!__any_sync(0xffffffffu, any_h)) continue;
                         const uint32_t hA = __reduce_and_sync(0xffffffffu, ha), hO = __reduce_or_sync(0xffffffffu, ho);
@@ -1266,7 +1287,32 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
         __syncthreads();
     }
     if (timer) { const unsigned long long t_ = clock64(); timer->r[6] += t_ - tr; tr = t_; }
-    if (left && tid < 32) {
+    if (left && left <= 64 && tid < 32) {
+        // a few undecided survivors left: warp 0 decides them one by one, in rank order, finding
+        // them 32 at a time by a ballot (lane t reads s_status[g0 + t]; lane 0 writes the decided
+        // one, which every lane re-reads only after the __syncwarp below)
+        for (uint32_t g0 = 0; g0 < Sc; g0 += 32) {
+          unsigned und = __ballot_sync(0xffffffffu, g0 + lane < Sc && s_status[g0 + lane] == 2);
+          __syncwarp();
+          while (und) {
+            const uint32_t j = g0 + (uint32_t)(__ffs(und) - 1);
+            und &= und - 1;
+            if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
+            const uint32_t cn = s_cnt[j];
+            bool acc_nb = false;
+            if (cn <= kPAdj) {
+                if (lane < cn) acc_nb = s_status[s_adj[j * kPAdj + lane]] == 1;
+            } else {
+                const uint32_t vj = s_val[j];
+                for (uint32_t k = lane; k < j; k += 32)
+                    acc_nb |= (s_status[k] == 1) && p_conflict(a, vj, s_val[k]);
+            }
+            acc_nb = __any_sync(0xffffffffu, acc_nb);
+            if (lane == 0) s_status[j] = acc_nb ? 0 : 1;
+            __syncwarp();
+          }
+        }
+    } else if (left && tid < 32) {
         // warp 0 finishes the undecided survivors group by group (32 consecutive ones, in rank
         // order): lane t owns survivor g0 + t.  A member is rejected by an accepted survivor
         // before the group (its conflict list, or a scan for an overflow node), else decided by
@@ -1277,7 +1323,7 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
             const uint32_t sj = in ? (uint32_t)s_status[j] : 0u;   // lane-owned until the write below
             const unsigned und = __ballot_sync(0xffffffffu, in && sj == 2);
             if (!und) continue;
-            if (a.timing && lane == 0) atomicAdd(&st->n_seq, (unsigned long long)__popc(und));
+            if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
             const uint32_t vj = in ? s_val[j] : 0u;
             const uint32_t cn = in ? s_cnt[j] : 0u;
             bool pre = false;
@@ -1355,7 +1401,7 @@ __device__ __forceinline__ uint32_t r_append(const PArgs &a, const PSmem &sm, ui
         const unsigned long long p0 = b & ~31ull;
         for (unsigned long long p = p0 + tid; p < ((e + 31) & ~31ull); p += blockDim.x) {
             const bool in = p >= b && p < e;
-            const uint32_t w = in ? s_stage[p - b] : 0u;
+            const uint32_t w = in ? p_ptag(a, s_stage[p - b]) : 0u;   // parity-tagged (a.par)
             const uint32_t an = __reduce_and_sync(0xffffffffu, in ? w : ~0u);
             const uint32_t orr = __reduce_or_sync(0xffffffffu, w);
             if (lane == 0) {

@@ -78,3 +78,62 @@ def test_weight_bound(seed):
         n = rng.randrange(1, 33)
         u, v = rng.getrandbits(n), rng.getrandbits(n)
         assert abs(popc(u) - popc(v)) <= popc(u ^ v)
+
+
+# ------------------------------------------------ parity refinement (a.par, n <= 30)
+
+def tagged(words):
+    # bit 31 = weight parity, as the parity-tagged summaries hold it (csrc/gc_screen.cuh p_ptag)
+    return [w | ((popc(w) & 1) << 31) for w in words]
+
+
+def parity_bound(block, cands, n):
+    """p_lbs: the block bound rounded up to the parity every distance must have when both sides
+    have a single weight parity (AND and OR agree in bit 31)."""
+    tb, tc = tagged(block), tagged(cands)
+    band, bor, cand, cor = 0xFFFFFFFF, 0, 0xFFFFFFFF, 0
+    for w in tb:
+        band &= w
+        bor |= w
+    for v in tc:
+        cand &= v
+        cor |= v
+    lb = popc(((band & ~cor) | (cand & ~bor)) & ((1 << n) - 1))
+    uniform = not (((band ^ bor) | (cand ^ cor)) >> 31) & 1
+    if uniform and (lb ^ ((bor ^ cor) >> 31)) & 1:
+        lb += 1
+    return lb
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_parity_bound_never_exceeds_min_distance(seed):
+    rng = random.Random(1000 + seed)
+    n = rng.choice([4, 7, 12, 20, 26, 30])
+    for _ in range(60):
+        # single-weight-class blocks and candidate batches (graded orders) and mixtures
+        wb, wc = rng.randrange(0, n + 1), rng.randrange(0, n + 1)
+
+        def word(weight):
+            if rng.random() < 0.7:
+                bits = rng.sample(range(n), weight)
+                return sum(1 << b for b in bits)
+            return rng.getrandbits(n)
+        block = [word(wb) for _ in range(rng.randrange(1, 33))]
+        cands = [word(wc) for _ in range(rng.randrange(1, 65))]
+        lb = parity_bound(block, cands, n)
+        dmin = min(popc(u ^ v) for u in block for v in cands)
+        assert lb <= dmin
+        assert lb >= block_bound(block, cands, n)
+
+
+def test_parity_bound_rounds_up():
+    # one weight class on each side: equal parities -> every distance even
+    n = 8
+    block = [0b00000111]                        # weight 3
+    cands = [0b01101000]                        # weight 3: distance 6
+    lb0 = block_bound(block, cands, n)
+    assert lb0 == 6 and parity_bound(block, cands, n) == 6
+    block = [0b00000111, 0b00001011]            # weight 3 (AND = 0b11)
+    cands = [0b00110001]                        # weight 3; plain bound 3 (odd) -> parity even -> 4
+    assert block_bound(block, cands, n) == 3
+    assert parity_bound(block, cands, n) == 4 == min(popc(b ^ cands[0]) for b in block)

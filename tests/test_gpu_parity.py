@@ -287,6 +287,7 @@ ENGINE_KNOBS = [
     {"geo_head": 64, "split_bits": 1},
     {"flags": 0x400},                           # no shared-memory super-block mirror
     {"flags": 0x800},                           # no preparing CTAs: the resolver does every tile
+    {"flags": 0x2000},                          # block bound without the parity refinement
     {"flags": 0x1000},                          # tile sizes from the survivors left after catch-up
     {"prep_lead": 1, "prep_ctas": 1},
     {"prep_lead": 6, "prep_ctas": 8, "pipeline_depth": 7},
