@@ -934,6 +934,8 @@ int pipeline_run(const RunArgs &r) {
                     "rounds %.2f sequential %.2f append %.2f stats %.2f publish %.2f us\n", f.t_level[9] / P / 1e3,
                     f.t_level[0] / P / c, f.t_level[1] / P / c, f.t_level[5] / P / c, f.t_level[6] / P / c,
                     f.t_level[2] / P / c, f.t_level[3] / P / c, f.t_level[4] / P / c, f.t_level[8] / P / c);
+            fprintf(stderr, "[gc]   tail: %llu chunks entered it (%.1f undecided threads each), %.2f us per tile in the tail "
+                    "itself\n", f.t_level[12], f.t_level[13] / (double)std::max(1ull, f.t_level[12]), f.t_r[7] / T / c);
             fprintf(stderr, "[gc]   per tile: survivors %.1f, accepted %.1f, resolve checks %.0f, levels %.2f; "
                     "largest S %llu, %llu multi-chunk tiles, %.2f rounds, %.2f sequential\n", f.survivors / T, f.M / T,
                     f.resolve_checks / T, f.levels / T, f.s_max, f.n_chunked, f.n_rounds / T, f.n_seq / T);

@@ -1287,6 +1287,10 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
         __syncthreads();
     }
     if (timer) { const unsigned long long t_ = clock64(); timer->r[6] += t_ - tr; tr = t_; }
+    if (a.timing && tid == 0 && left) {          // diagnostics: tiles entering the tail, undecided threads
+        atomicAdd(&st->t_level[12], 1ull);
+        atomicAdd(&st->t_level[13], (unsigned long long)left);
+    }
     if (left && left <= 64 && tid < 32) {
         // a few undecided survivors left: warp 0 decides them one by one, in rank order, finding
         // them 32 at a time by a ballot (lane t reads s_status[g0 + t]; lane 0 writes the decided
@@ -1315,50 +1319,63 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
     } else if (left && tid < 32) {
         // warp 0 finishes the undecided survivors group by group (32 consecutive ones, in rank
         // order): lane t owns survivor g0 + t.  A member is rejected by an accepted survivor
-        // before the group (its conflict list, or a scan for an overflow node), else decided by
-        // the group's own greedy over a 32 x 32 conflict bit matrix held in registers.
+        // before the group -- its conflict list, or, for an overflow node (more conflicts than the
+        // list holds), the values of the accepted survivors so far, kept in order in s_tmp (free
+        // after the prior checks) -- else decided by the group's own greedy over a 32 x 32
+        // conflict bit matrix held in registers.
+        const bool use_list = Sc <= sm.tmp_words;
+        uint32_t n_acc = 0;                                // accepted survivors before g0 (use_list)
         for (uint32_t g0 = 0; g0 < Sc; g0 += 32) {
             const uint32_t j = g0 + lane;
             const bool in = j < Sc;
             const uint32_t sj = in ? (uint32_t)s_status[j] : 0u;   // lane-owned until the write below
-            const unsigned und = __ballot_sync(0xffffffffu, in && sj == 2);
-            if (!und) continue;
-            if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
             const uint32_t vj = in ? s_val[j] : 0u;
-            const uint32_t cn = in ? s_cnt[j] : 0u;
-            bool pre = false;
-            if (sj == 2 && cn <= kPAdj)
-                for (uint32_t t = 0; t < cn; ++t) {
-                    const uint32_t k = s_adj[j * kPAdj + t];
-                    pre |= k < g0 && s_status[k] == 1;
-                }
-            unsigned ovm = __ballot_sync(0xffffffffu, sj == 2 && cn > kPAdj);
-            while (ovm) {                                  // overflow nodes: the warp scans for them
-                const int t = __ffs(ovm) - 1;
-                ovm &= ovm - 1;
-                const uint32_t vt = __shfl_sync(0xffffffffu, vj, t);
-                bool c = false;
-                for (uint32_t k = lane; k < g0; k += 32) c |= s_status[k] == 1 && p_conflict(a, vt, s_val[k]);
-                c = __any_sync(0xffffffffu, c);
-                if (lane == t) pre |= c;
-            }
-            uint32_t inmask = 0;                           // earlier members of the group in conflict
-#pragma unroll
-            for (int t = 0; t < 32; ++t) {
-                const uint32_t vt = __shfl_sync(0xffffffffu, vj, t);
-                if (t < lane && p_conflict(a, vj, vt)) inmask |= 1u << t;
-            }
-            const unsigned prem = __ballot_sync(0xffffffffu, pre);
+            const unsigned und = __ballot_sync(0xffffffffu, in && sj == 2);
             unsigned acc = __ballot_sync(0xffffffffu, in && sj == 1);
+            if (und) {
+                if (a.timing && lane == 0) atomicAdd(&st->n_seq, 1ull);
+                const uint32_t cn = in ? s_cnt[j] : 0u;
+                bool pre = false;
+                if (sj == 2 && cn <= kPAdj) {
+                    for (uint32_t t = 0; t < cn; ++t) {
+                        const uint32_t k = s_adj[j * kPAdj + t];
+                        pre |= k < g0 && s_status[k] == 1;
+                    }
+                } else if (sj == 2 && use_list) {          // overflow node: the accepted list, newest first
+                    for (uint32_t k = n_acc; k > 0 && !pre; --k) pre = p_conflict(a, vj, sm.s_tmp[k - 1]);
+                }
+                unsigned ovm = use_list ? 0u : __ballot_sync(0xffffffffu, sj == 2 && cn > kPAdj);
+                while (ovm) {                              // (no room for the list) the warp scans
+                    const int t = __ffs(ovm) - 1;
+                    ovm &= ovm - 1;
+                    const uint32_t vt = __shfl_sync(0xffffffffu, vj, t);
+                    bool c = false;
+                    for (uint32_t k = lane; k < g0; k += 32) c |= s_status[k] == 1 && p_conflict(a, vt, s_val[k]);
+                    c = __any_sync(0xffffffffu, c);
+                    if (lane == t) pre |= c;
+                }
+                uint32_t inmask = 0;                       // earlier members of the group in conflict
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-                const uint32_t im = __shfl_sync(0xffffffffu, inmask, t);
-                if (((und & ~prem) >> t & 1u) && !(im & acc)) acc |= 1u << t;
+                for (int t = 0; t < 32; ++t) {
+                    const uint32_t vt = __shfl_sync(0xffffffffu, vj, t);
+                    if (t < lane && p_conflict(a, vj, vt)) inmask |= 1u << t;
+                }
+                const unsigned prem = __ballot_sync(0xffffffffu, pre);
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const uint32_t im = __shfl_sync(0xffffffffu, inmask, t);
+                    if (((und & ~prem) >> t & 1u) && !(im & acc)) acc |= 1u << t;
+                }
+                if (sj == 2) s_status[j] = (acc >> lane & 1u) ? 1 : 0;
             }
-            if (sj == 2) s_status[j] = (acc >> lane & 1u) ? 1 : 0;
+            if (use_list) {                                // the group's accepted members, in order
+                if (acc >> lane & 1u) sm.s_tmp[n_acc + __popc(acc & ((1u << lane) - 1u))] = vj;
+                n_acc += __popc(acc);
+            }
             __syncwarp();
         }
     }
+    if (timer) { const unsigned long long t_ = clock64(); timer->r[7] += t_ - tr; }
     __syncthreads();
     if (timer) { const unsigned long long t_ = clock64(); timer->r[2] += t_ - tr; tr = t_; }
 }
