@@ -569,7 +569,7 @@ int persistent_run_partitioned(const RunArgs &r) {
     const unsigned G = r.world > 1 ? (unsigned)r.world : r.opt.emulate_ranks;
     const unsigned parts_local = r.world > 1 ? 1u : G;
     a.part_mode = 1;
-    a.chunk = 4096u;
+    a.chunk = 2048u;
     const uint32_t tile_max = r.opt.tile_max ? r.opt.tile_max : 16384u;
     const size_t smem = p_dyn_smem(a.chunk);
     PCK(cudaFuncSetAttribute((const void *)k_construct<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

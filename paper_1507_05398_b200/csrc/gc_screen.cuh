@@ -28,7 +28,7 @@ constexpr uint32_t kPTargetAccepted = 384;  // adaptive tiles grow up to ~2x thi
                                             // (Gray: twice that, graded orders: four times;
                                             // tools/sweep_knobs2.sh, profiles/r01j_knob_sweep.md)
 constexpr uint32_t kPMaxPredictedSurvivors = 1024;
-constexpr int kPAdj = 16;                       // earlier in-tile conflicts recorded per survivor
+constexpr int kPAdj = 32;                       // earlier in-tile conflicts recorded per survivor
 constexpr uint32_t kPStageWords = 32 * 32;      // per-warp stage: 32 blocks of 32 codewords (4 KiB)
 constexpr uint32_t kPWarpStage = kPStageWords + 8 * 64 + 32;   // + 8 super-blocks' block summaries + a block queue
 constexpr uint32_t kPWinWords = 16384 + 32;     // level-0 window copied to shared memory (words, then
