@@ -142,6 +142,17 @@ typedef struct gc_options {
                                         when a block's codewords and a warp's candidates each have one
                                         weight parity, the bound rounds up to the parity of every
                                         distance)                                                    */
+#define GC_FLAG_CROSS          0x4000u /* pipelined engine: two-stage preparation -- stage A (survivors, their
+                                        check against the committed words, in-tile conflict lists) once
+                                        a tile is screened, stage B one tile ahead of the resolver: the
+                                        words committed since, and the conflicts with the previous
+                                        tile's prepared list (cross lists), so the resolver checks no
+                                        committed word (default off)                                */
+#define GC_FLAG_NO_CATCHUP     0x8000u /* pipelined engine: no catch-up screening level (default for graded
+                                        orders and d = 4: after its window levels a tile's live
+                                        candidates are screened against the words committed since its
+                                        descriptor, so fewer survivors reach the preparation)        */
+#define GC_FLAG_CATCHUP        0x10000u /* pipelined engine: the catch-up level for every ordering          */
 #define GC_FLAG_KERNEL_TIMING  0x8u  /* bracket every screen launch with CUDA events on the launching
                                         stream; fills gc_stats.screen_ms (benchmarking)               */
 

@@ -23,6 +23,9 @@ from ._binding import (  # noqa: F401
     GC_FLAG_NO_PREP,
     GC_FLAG_SIZE_ON_TRUE,
     GC_FLAG_NO_PARITY_BOUND,
+    GC_FLAG_CROSS,
+    GC_FLAG_NO_CATCHUP,
+    GC_FLAG_CATCHUP,
     GC_FLAG_DEBUG_PHASES,
     GC_FLAG_NO_SUP_SMEM,
     GC_B_ORDERING,

@@ -31,6 +31,9 @@ GC_FLAG_TILE_BARRIERS = 0x100
 GC_FLAG_NO_PREP = 0x800
 GC_FLAG_SIZE_ON_TRUE = 0x1000
 GC_FLAG_NO_PARITY_BOUND = 0x2000
+GC_FLAG_CROSS = 0x4000
+GC_FLAG_NO_CATCHUP = 0x8000
+GC_FLAG_CATCHUP = 0x10000
 GC_FLAG_DEBUG_PHASES = 0x200
 GC_FLAG_NO_SUP_SMEM = 0x400
 

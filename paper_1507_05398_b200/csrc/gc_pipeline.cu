@@ -44,19 +44,23 @@ constexpr unsigned long long kQStallNs = 30ull * 1000 * 1000 * 1000;
 // QSlot::prep packs everything the resolver needs from a preparation into one word, so that
 // its CAS (or the poll that sees it finished) is the only round trip:
 //   tag (tile + 1, 12 bits) << 52 | state << 50 | (M_prep - M_s) (21 bits) << 29
-//     | S_prep (13 bits) << 16 | survivors of the screen (16 bits, saturated)
-// (M_prep - M_s counts the words committed since the tile's screen: < depth tiles x 2^16)
+//     | S_prep (13 bits) << 16 | xb (3 bits) << 13 | survivors of the screen (13 bits, saturated)
+// (M_prep - M_s counts the words committed since the tile's screen: < depth tiles x 2^16; xb > 0:
+// cross lists recorded against the prepared lists of the xb tiles before this one, which were
+// not committed when the preparation read M_prep)
 constexpr unsigned kPrepOpen = 0, kPrepBusy = 1, kPrepDone = 2, kPrepResolver = 3;
 constexpr uint32_t kPrepTooMany = 0x1fff;           // S_prep: more survivors than one resolve chunk
 __host__ __device__ constexpr unsigned long long q_pw(unsigned long long i, unsigned st, unsigned long long dM = 0,
-                                                      uint32_t S = 0, uint32_t S_screen = 0) {
+                                                      uint32_t S = 0, uint32_t S_screen = 0, uint32_t xb = 0) {
     return (((i + 1) & 0xfffull) << 52) | ((unsigned long long)st << 50) | (dM << 29) |
-           ((unsigned long long)S << 16) | (S_screen > 0xffffu ? 0xffffu : S_screen);
+           ((unsigned long long)S << 16) | ((unsigned long long)(xb & 7u) << 13) |
+           (S_screen > 0x1fffu ? 0x1fffu : S_screen);
 }
 __device__ __forceinline__ unsigned q_pw_state(unsigned long long w) { return (unsigned)(w >> 50) & 3u; }
 __device__ __forceinline__ unsigned long long q_pw_dM(unsigned long long w) { return (w >> 29) & ((1ull << 21) - 1); }
 __device__ __forceinline__ uint32_t q_pw_S(unsigned long long w) { return (uint32_t)(w >> 16) & 0x1fffu; }
-__device__ __forceinline__ uint32_t q_pw_Sscreen(unsigned long long w) { return (uint32_t)(w & 0xffffu); }
+__device__ __forceinline__ uint32_t q_pw_xb(unsigned long long w) { return (uint32_t)(w >> 13) & 7u; }
+__device__ __forceinline__ uint32_t q_pw_Sscreen(unsigned long long w) { return (uint32_t)(w & 0x1fffu); }
 
 // One tile in flight (global memory).  The descriptor fields are written by the resolver before
 // it releases `phase`; `items[l]` / `nlive[l]` for l >= 1 by the warp that finished level l - 1
@@ -65,10 +69,14 @@ __device__ __forceinline__ uint32_t q_pw_Sscreen(unsigned long long w) { return 
 struct QSlot {
     unsigned long long phase;                   // (tile + 1) << 8 | level; level >= L: screened
     unsigned long long prep;                    // q_pw(tile, state, M_prep, S_prep)
+    unsigned long long t_pub, t_scr;            // diagnostics (timing): descriptor published, screen done
+    unsigned long long listw;                   // (tile + 1) << 16 | S_prep (0xffff: none): the prepared
+                                                // list, published before the cross step (cross lists)
     unsigned long long t0, M_s, base;           // first rank; screened against codebook[base, M_s)
     uint32_t K, L;                              // candidates; levels
     unsigned int inside;                        // CTAs between validating a level and their last claim
-    uint32_t pad;
+    uint32_t cu;                                // 1: level L - 1 is the catch-up level over codebook[M_s, M_x)
+    unsigned long long M_x;                     // catch-up: end of its window (set when the level opens)
     uint32_t items[kPMaxLevels];                // warp items of each level
     uint32_t nlive[kPMaxLevels];                // live candidates at the start of each level
     uint32_t done[kPMaxLevels];                 // items finished (arrival counter)
@@ -83,6 +91,12 @@ struct QCtl {
     unsigned long long preps, prep_used;        // diagnostics: tiles prepared / resolved from a prep
     unsigned long long prep_rchk;               // resolve checks done by preparations
     unsigned long long busy_prep_ns;            // diagnostics: resolver busy time on prepared tiles
+    unsigned long long n_xmode;                 // diagnostics (timing): tiles resolved in cross mode
+    unsigned long long prep_ns, xcross_ns, n_xb;              // diagnostics (timing): stage A time, stage B
+                                                // time, stage B count
+    unsigned long long arr[4], scr_ns, lag_ns, n_scr;        // diagnostics (timing): resolver arrivals at a tile
+                                                // unscreened / screened but open / prep busy / prep done;
+                                                // publish -> screened; screened -> resolver arrival
     QSlot slot[kQRing];
 };
 
@@ -188,6 +202,20 @@ __device__ __forceinline__ void q_reset(QCtl *q, unsigned long long i, unsigned 
     for (int l = 0; l < kPMaxLevels; ++l) { sl.claim[l] = tag << 32; sl.done[l] = 0; }
 }
 
+// Levels of a tile screened against codebook[base, M_s): the window levels, plus (pipelined engine,
+// one rank, GC_FLAG_NO_CATCHUP off) a last catch-up level over the words committed meanwhile.
+__device__ __forceinline__ int q_levels(const PArgs &a, unsigned long long M_s, unsigned long long base, uint32_t &cu) {
+    const int L = p_levels(M_s - base, a.W0, a.growth);
+    cu = (a.cm && a.world <= 1 && L > 0 && L < kPMaxLevels) ? 1u : 0u;
+    return L + (int)cu;
+}
+// window [lo, hi) of level l of a tile with L levels (cu, M_x: its catch-up level)
+__device__ __forceinline__ void q_level_window(const PArgs &a, unsigned long long M_s, unsigned long long base, int L,
+                                               uint32_t cu, unsigned long long M_x, int l, long long &hi, long long &lo) {
+    if (cu && l == L - 1) { hi = (long long)M_x; lo = (long long)M_s; return; }
+    p_level_window(a, M_s, base, L - (int)cu, l, hi, lo);
+}
+
 // Resolver thread 0: write the descriptor of tile i (ranks [t0, t0 + K)) to be screened against
 // codebook[base, M_s) into its (reset) slot.  Level 0 plans all K candidates; a tile with nothing
 // to screen (L == 0) is published as already screened.  Returns the phase word; the caller makes
@@ -196,13 +224,15 @@ __device__ __forceinline__ unsigned long long q_write(const PArgs &a, QCtl *q, u
                                                       unsigned long long t0, uint32_t K, unsigned long long M_s,
                                                       unsigned long long base) {
     QSlot &sl = q->slot[i % kQRing];
-    const int L = p_levels(M_s - base, a.W0, a.growth);
+    uint32_t cu;
+    const int L = q_levels(a, M_s, base, cu);
     sl.t0 = t0; sl.K = K; sl.M_s = M_s; sl.base = base; sl.L = (uint32_t)L;
+    sl.cu = cu; sl.M_x = 0;
     uint32_t plo, n0;
     q_part(a, K, plo, n0);
     if (L > 0 && n0 > 0) {
         long long hi, lo;
-        p_level_window(a, M_s, base, L, 0, hi, lo);
+        p_level_window(a, M_s, base, L - (int)cu, 0, hi, lo);
         sl.items[0] = (uint32_t)p_plan(a, n0, hi - lo, a.plan_warps).items();
         sl.nlive[0] = n0;
     }
@@ -238,10 +268,21 @@ __device__ __forceinline__ void q_finish_level(const PArgs &a, QSlot *sl, unsign
     live = __reduce_add_sync(0xffffffffu, live);
     int nl = l + 1;
     uint32_t items = 0;
+    const uint32_t cu = __ldcg(&sl->cu);
     if (nl < L && live > 0) {
         long long hi, lo;
-        p_level_window(a, M_s, base, L, nl, hi, lo);
-        items = (uint32_t)p_plan(a, live, hi - lo, a.plan_warps).items();
+        if (cu && nl == L - 1) {
+            // the catch-up level: the words committed since the descriptor (read now), so that the
+            // preparation and the resolver check the survivors against fewer of them
+            unsigned long long mx = 0;
+            if (lane == 0) mx = q_ld_acquire(a.cm) & kQM;
+            mx = __shfl_sync(0xffffffffu, mx, 0);
+            hi = (long long)mx; lo = (long long)M_s;
+            if (lane == 0) sl->M_x = mx;
+        } else {
+            p_level_window(a, M_s, base, L - (int)cu, nl, hi, lo);
+        }
+        if (hi > lo) items = (uint32_t)p_plan(a, live, hi - lo, a.plan_warps).items();
     }
     if (items == 0) nl = L;                           // nothing left to screen
     __syncwarp();
@@ -251,10 +292,57 @@ __device__ __forceinline__ void q_finish_level(const PArgs &a, QSlot *sl, unsign
             sl->items[nl] = items;
             sl->nlive[nl] = live;
         }
+        if (a.timing && nl >= L) sl->t_scr = p_now();
         __threadfence();
         q_st_relaxed(&sl->phase, ((i + 1) << 8) | (unsigned)nl);
     }
     __syncwarp();
+}
+
+// Stage B of a preparation (cross lists), run by a preparing CTA on tile j = com + 1 while tile
+// com is being resolved; stage A (p_prep, any time after the screen) left the tile's survivors
+// checked against codebook[0, M_cA) in its prep buffer and published them as its list (word w).
+// Stage B flags the survivors in conflict with the words committed since, codebook[M_cA, M_cB)
+// (M_cB: the codebook after tile com - 1), and records their conflicts with the list of tile com
+// -- a superset of the words tile com will add, at the positions the resolver decides it in
+// (cross lists, kPX per survivor; xcnt = 0xff: flagged).  The resolver then needs no check
+// against committed words at all.  Returns the new prep word: xb = 1 (M_prep = M_cB), or xb = 7
+// when a survivor has more than kPX cross conflicts (the flags are kept, the cross lists are not
+// used: the resolver checks codebook[M_cA, M) itself).  Ends with a barrier.
+__device__ __forceinline__ unsigned long long q_stage_b(const PArgs &a, const PSmem &sm, unsigned long long j,
+                                                        unsigned long long w, unsigned long long M_s,
+                                                        unsigned long long M_cB, uint32_t S_prev, uint8_t *buf,
+                                                        unsigned long long &rchk) {
+    __shared__ XList s_xl[1];
+    __shared__ int s_ovf;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t S = q_pw_S(w);
+    const unsigned long long M_cA = M_s + q_pw_dM(w);
+    const uint32_t *val = reinterpret_cast<const uint32_t *>(buf);
+    uint16_t *xadj = reinterpret_cast<uint16_t *>(buf + p_prep_xadj(sm.chunk));
+    uint8_t *xcnt = buf + p_prep_xcnt(sm.chunk);
+    for (uint32_t k = tid; k < S; k += blockDim.x) {
+        sm.s_val[k] = __ldcg(val + k);
+        sm.s_cnt[k] = 0;
+    }
+    if (tid == 0) {
+        s_ovf = 0;
+        s_xl[0].val = reinterpret_cast<const uint32_t *>(a.qprep + (size_t)((j - 1) % kQRing) * p_prep_bytes(sm.chunk));
+        s_xl[0].S = S_prev;
+    }
+    __syncthreads();
+    r_consensus(sm, S);
+    r_prior(a, sm, S, M_cA, M_cB > M_cA ? M_cB : M_cA, false, rchk);   // s_status: flagged (zeroed first)
+    if (S_prev) r_cross(a, sm, S, s_xl, 1, xadj, rchk);
+    for (uint32_t k = tid; k < S; k += blockDim.x) {
+        const uint32_t c = sm.s_cnt[k];
+        const bool flagged = sm.s_status[k] != 0;
+        if (!flagged && c > (uint32_t)kPX) s_ovf = 1;
+        __stcg(xcnt + k, flagged ? (uint8_t)0xff : (uint8_t)min(c, 254u));
+    }
+    __syncthreads();
+    return s_ovf ? q_pw(j, kPrepDone, q_pw_dM(w), S, q_pw_Sscreen(w), 7)
+                 : q_pw(j, kPrepDone, (M_cB > M_cA ? M_cB : M_cA) - M_s, S, q_pw_Sscreen(w), 1);
 }
 
 // the resolve scratch of a CTA in the dynamic shared memory (the level stages alias it)
@@ -305,7 +393,11 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
         __shared__ uint32_t s_K[kQRing], s_L[kQRing];
         __shared__ unsigned long long s_next, s_issued;
         __shared__ int s_mode;
+        __shared__ unsigned long long s_plo;             // mode 0: survivors screened against codebook[0, s_plo)
         __shared__ PPrep s_pp;
+        __shared__ uint32_t s_xbits[kPXRing][64];        // accepted positions of the last tiles' lists
+        __shared__ unsigned long long s_listed[kPXRing]; // tile + 1 when resolved from its prepared list
+        if (threadIdx.x < kPXRing) s_listed[threadIdx.x] = 0;
         const bool pre_reset = a.depth < kQRing;         // slot of tile i + D reset during tile i
         if (threadIdx.x == 0) {
             p_count_load(pc, st);
@@ -340,65 +432,91 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
             QSlot *sl = &q->slot[si];
             if (threadIdx.x == 0) {
                 const unsigned long long tw = p_now();
-                if (pre_reset && s_next < a.t_end) q_reset(q, i + a.depth, i ? in_ahead : 1u);
-                // Prepared by another CTA?  One CAS: it either hands over the finished preparation
-                // or takes the tile over (nobody started on it: this CTA does all of it).
-                int mode = 0;
-                bool need_phase = true;
-                if (a.prep_lead > 0) {
-                    const unsigned long long open = q_pw(i, kPrepOpen, 0, 0);
-                    // the word read (acquire) while the previous commit was being published: a
-                    // finished preparation is final, anything else needs the CAS
-                    unsigned long long w = w_ahead;
-                    if (!(w >> 52 == ((i + 1) & 0xfffull) && q_pw_state(w) == kPrepDone))
-                        w = q_cas_acqrel(&sl->prep, open, q_pw(i, kPrepResolver, 0, 0));
-                    if (w != open) {
-                        while (q_pw_state(w) != kPrepDone) {
+                {
+                    if (a.timing) {      // what the resolver finds on arrival
+                        const unsigned long long ph = q_ld_acquire(&sl->phase), pw = q_ld_acquire(&sl->prep);
+                        const bool scr = (ph >> 8) == i + 1 && (uint32_t)(ph & 0xff) >= s_L[si];
+                        const unsigned ps = q_pw_state(pw);
+                        q->arr[!scr ? 0 : ps == kPrepOpen ? 1 : ps == kPrepBusy ? 2 : 3]++;
+                        const unsigned long long ts = __ldcg(&sl->t_scr), tpb = __ldcg(&sl->t_pub);
+                        if (scr && ts && tpb && ts > tpb) { q->scr_ns += ts - tpb; q->lag_ns += tw > ts ? tw - ts : 0; q->n_scr++; }
+                    }
+                    if (pre_reset && s_next < a.t_end) q_reset(q, i + a.depth, i ? in_ahead : 1u);
+                    // Prepared by another CTA?  One CAS: it either hands over the finished preparation
+                    // or takes the tile over (nobody started on it: this CTA does all of it).
+                    int mode = 0;
+                    bool need_phase = true;
+                    if (a.prep_lead > 0) {
+                        const unsigned long long open = q_pw(i, kPrepOpen, 0, 0);
+                        // the word read (acquire) while the previous commit was being published: a
+                        // finished preparation is final, anything else needs the CAS
+                        unsigned long long w = w_ahead;
+                        if (!(w >> 52 == ((i + 1) & 0xfffull) && q_pw_state(w) == kPrepDone))
+                            w = q_cas_acqrel(&sl->prep, open, q_pw(i, kPrepResolver, 0, 0));
+                        if (w != open) {
+                            while (q_pw_state(w) != kPrepDone) {
+                                __nanosleep(32);
+                                w = q_ld_acquire(&sl->prep);
+                                if (p_now() - tw > kQStallNs) { s_stall = 1; break; }
+                            }
+                            need_phase = false;               // prepared implies screened
+                            if (q_pw_S(w) != kPrepTooMany) {
+                                const uint8_t *buf = a.qprep + (size_t)si * p_prep_bytes(kPChunk);
+                                s_pp.S = q_pw_S(w);
+                                s_pp.S_screen = q_pw_Sscreen(w);
+                                s_pp.M_prep = s_Ms[si] + q_pw_dM(w);
+                                s_pp.val = reinterpret_cast<const uint32_t *>(buf);
+                                s_pp.cnt = reinterpret_cast<const uint32_t *>(buf + (size_t)kPChunk * 4);
+                                s_pp.idx = reinterpret_cast<const uint16_t *>(buf + (size_t)kPChunk * 8);
+                                s_pp.adj = reinterpret_cast<const uint16_t *>(buf + (size_t)kPChunk * 10);
+                                s_pp.xcnt = buf + p_prep_xcnt(kPChunk);
+                                s_pp.xadj = reinterpret_cast<const uint16_t *>(buf + p_prep_xadj(kPChunk));
+                                s_pp.xbits = s_xbits;
+                                s_pp.tile = i;
+                                // stage B ran (xb 1 or 7): xcnt flags the survivors in conflict with
+                                // codebook[M_cA, M_prep); cross mode (xb 1): the tile before was
+                                // resolved from its list (then codebook[M_prep, M) are exactly its
+                                // accepted words, and the cross lists say which survivors they reject)
+                                const uint32_t xb = q_pw_xb(w);
+                                s_pp.xstage = xb != 0;
+                                const bool xm = xb == 1 && i >= 1 && s_listed[(i - 1) % kPXRing] == i;
+                                s_pp.xmode = xm;
+                                if (xm && a.timing) q->n_xmode++;
+                                mode = 1;
+                                ++n_used;
+                            }
+                        }
+                    }
+                    if (need_phase) {
+                        for (;;) {
+                            const unsigned long long ph = q_ld_acquire(&sl->phase);
+                            if ((ph >> 8) == i + 1 && (uint32_t)(ph & 0xff) >= s_L[si] && q_peers_in(a, si, i)) break;
                             __nanosleep(32);
-                            w = q_ld_acquire(&sl->prep);
                             if (p_now() - tw > kQStallNs) { s_stall = 1; break; }
                         }
-                        need_phase = false;               // prepared implies screened
-                        if (q_pw_S(w) != kPrepTooMany) {
-                            const uint8_t *buf = a.qprep + (size_t)si * p_prep_bytes(kPChunk);
-                            s_pp.S = q_pw_S(w);
-                            s_pp.S_screen = q_pw_Sscreen(w);
-                            s_pp.M_prep = s_Ms[si] + q_pw_dM(w);
-                            s_pp.val = reinterpret_cast<const uint32_t *>(buf);
-                            s_pp.cnt = reinterpret_cast<const uint32_t *>(buf + (size_t)kPChunk * 4);
-                            s_pp.idx = reinterpret_cast<const uint16_t *>(buf + (size_t)kPChunk * 8);
-                            s_pp.adj = reinterpret_cast<const uint16_t *>(buf + (size_t)kPChunk * 10);
-                            mode = 1;
-                            ++n_used;
-                        }
                     }
+                    s_mode = mode;
+                    // the screen covered codebook[0, M_x) when its catch-up level ran
+                    s_plo = max(s_Ms[si], __ldcg(&sl->cu) ? __ldcg(&sl->M_x) : 0ull);
+                    const unsigned long long tb = p_now();
+                    if (mode) t_top_p += tb - tw;
+                    t_wait += tb - tw;
+                    t_busy -= tb;
+                    tb0 = tb;
                 }
-                if (need_phase) {
-                    for (;;) {
-                        const unsigned long long ph = q_ld_acquire(&sl->phase);
-                        if ((ph >> 8) == i + 1 && (uint32_t)(ph & 0xff) >= s_L[si] && q_peers_in(a, si, i)) break;
-                        __nanosleep(32);
-                        if (p_now() - tw > kQStallNs) { s_stall = 1; break; }
-                    }
-                }
-                s_mode = mode;
-                const unsigned long long tb = p_now();
-                if (mode) t_top_p += tb - tw;
-                t_wait += tb - tw;
-                t_busy -= tb;
-                tb0 = tb;
             }
             __syncthreads();
             if (s_stall) break;          // watchdog: a screen, a preparation or a peer never arrived
             uint32_t *dead = a.qdead + (size_t)si * kQWords;
             if (timer)
                 for (int k = 0; k < 8; ++k) t_r0[k] = tmr.r[k];
-            p_resolve(a, sm, s_t0[si], s_K[si], (int)s_L[si], pc, timer, 0, false, dead, s_Ms[si],
-                      s_mode ? &s_pp : nullptr);
+            p_resolve(a, sm, s_t0[si], s_K[si], (int)s_L[si], pc, timer, 0, false, dead, s_plo,
+                      s_mode ? &s_pp : nullptr, (s_mode && a.cross) ? s_xbits[i % kPXRing] : nullptr);
             if (timer && s_mode)
                 for (int k = 0; k < 8; ++k) t_rp[k] += tmr.r[k] - t_r0[k];
             if (threadIdx.x == 0) {
                 const unsigned long long tp = timer ? clock64() : 0;
+                s_listed[i % kPXRing] = s_mode ? i + 1 : 0;
                 // next descriptor: tile s_issued, screened against the codebook as of now; its
                 // size follows the tile just resolved (p_resolve's pc.K_next)
                 unsigned long long ph = 0, *php = nullptr;
@@ -409,8 +527,10 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                     const int sj = (int)(s_issued % kQRing);
                     if (!pre_reset) q_reset(q, s_issued);
                     s_t0[sj] = s_next; s_K[sj] = Kn; s_Ms[sj] = pc.M;
-                    s_L[sj] = (uint32_t)p_levels(pc.M - base, a.W0, a.growth);
+                    uint32_t cu_;
+                    s_L[sj] = (uint32_t)q_levels(a, pc.M, base, cu_);
                     ph = q_write(a, q, s_issued, s_next, Kn, pc.M, base);
+                    if (a.timing) { q->slot[sj].t_pub = p_now(); q->slot[sj].t_scr = 0; }
                     php = &q->slot[sj].phase;
                     s_next += Kn;
                     ++s_issued;
@@ -458,19 +578,42 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
         // CTAs 1 .. prep_ctas only prepare tiles for the resolver; the others screen, and prepare
         // too when a tile is ready and they are between levels.
         const bool prep_only = bid <= a.prep_ctas;
-        __shared__ unsigned long long s_tile, s_t0, s_Ms, s_base, s_Mc;
-        __shared__ uint32_t s_K, s_L;
-        __shared__ int s_lvl;                 // >= 0: a level; -2: finished; -3: prepare s_tile
+        __shared__ unsigned long long s_tile, s_t0, s_Ms, s_base, s_Mc, s_wA;
+        __shared__ uint32_t s_K, s_L, s_Sprev, s_cu;
+        __shared__ unsigned long long s_Mx;
+        __shared__ int s_lvl;                 // >= 0: a level; -2: finished; -3: prepare s_tile (stage A); -4: stage B
         unsigned long long hint = 0, supM = 0, n_prep = 0;
         for (;;) {
             if (threadIdx.x == 0) {
                 int lvl = -1;
-                unsigned long long pick = 0, Mc = 0;
+                unsigned long long pick = 0, Mc = 0, c0 = 0;
+                uint32_t sprev = 0;
                 unsigned int nap = 32;
                 for (;;) {
                     const unsigned long long cmv = q_ld_acquire(&q->cm);
                     const unsigned long long com = cmv >> 40;
-                    // 1. prepare a screened tile the resolver reaches soon (its critical path)
+                    // 0. stage B of the tile after the one being resolved (the resolver's next tile)
+                    if (a.cross) {
+                        const unsigned long long j = com + 1;
+                        QSlot *sl = &q->slot[j % kQRing];
+                        const unsigned long long w = q_ld_acquire(&sl->prep);
+                        if ((w >> 52) == ((j + 1) & 0xfffull) && q_pw_state(w) == kPrepDone && q_pw_xb(w) == 0 &&
+                            q_pw_S(w) != kPrepTooMany && q_pw_S(w) != 0) {
+                            const unsigned long long lw = q_ld_acquire(&q->slot[com % kQRing].listw);
+                            if ((lw >> 16) == com + 1 && (lw & 0xffffu) != 0xffffu) {
+                                const unsigned long long wb = (w & ~(3ull << 50)) | ((unsigned long long)kPrepBusy << 50);
+                                if (atomicCAS(&sl->prep, w, wb) == w) {
+                                    pick = j;
+                                    Mc = cmv & kQM;
+                                    c0 = w;
+                                    sprev = (uint32_t)(lw & 0xffffu);
+                                    lvl = -4;
+                                    break;
+                                }
+                            }
+                        }
+                    }
+                    // 1. prepare (stage A) a screened tile the resolver reaches soon
                     for (unsigned long long j = com + 1; a.prep_lead > 0 && j <= com + (unsigned long long)a.prep_lead &&
                                                          j < com + (unsigned long long)a.depth; ++j) {
                         QSlot *sl = &q->slot[j % kQRing];
@@ -511,18 +654,21 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                             atomicSub(&sl->inside, 1u);
                         }
                     }
-                    if (lvl >= 0) break;
+                    if (lvl >= 0 || lvl == -4) break;
                     if (q_ld_acquire32(&q->finished)) { lvl = -2; break; }
                     __nanosleep(nap);
                     if (nap < (prep_only ? 64u : 512u)) nap *= 2;
                 }
                 s_lvl = lvl;
-                if (lvl >= 0 || lvl == -3) {
+                if (lvl >= 0 || lvl <= -3) {
                     QSlot *sl = &q->slot[pick % kQRing];
                     s_tile = pick;
                     s_t0 = __ldcg(&sl->t0); s_Ms = __ldcg(&sl->M_s); s_base = __ldcg(&sl->base);
                     s_K = __ldcg(&sl->K); s_L = __ldcg(&sl->L);
+                    s_cu = __ldcg(&sl->cu); s_Mx = __ldcg(&sl->M_x);
                     s_Mc = Mc;
+                    s_wA = c0;
+                    s_Sprev = sprev;
                 }
             }
             __syncthreads();
@@ -534,13 +680,33 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
             const int si = (int)(i % kQRing);
             QSlot *sl = &q->slot[si];
             uint32_t *dead = a.qdead + (size_t)si * kQWords, *kill = a.qkill + (size_t)si * kQWords;
+            if (l == -4) {
+                // ---- stage B of tile i (the resolver's next tile)
+                unsigned long long rchk = 0;
+                const unsigned long long tp0 = a.timing ? p_now() : 0;
+                const unsigned long long wn = q_stage_b(a, sm, i, s_wA, M_s, s_Mc, s_Sprev,
+                                                        a.qprep + (size_t)si * p_prep_bytes(kPChunk), rchk);
+                for (int o = 16; o > 0; o >>= 1) rchk += __shfl_down_sync(0xffffffffu, rchk, o);
+                if (lane == 0 && rchk) atomicAdd(&q->prep_rchk, rchk);
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    // (a CAS: the slot is never rewritten under a stage B, but do not rely on timing)
+                    atomicCAS(&sl->prep, (s_wA & ~(3ull << 50)) | ((unsigned long long)kPrepBusy << 50), wn);
+                    if (a.timing) { atomicAdd(&q->xcross_ns, p_now() - tp0); atomicAdd(&q->n_xb, 1ull); }
+                }
+                continue;
+            }
             if (l == -3) {
                 // ---- prepare tile i for the resolver
                 unsigned long long rchk = 0;
                 uint32_t S1 = 0;
-                const uint32_t S2 = p_prep(a, sm, t0, K, L, dead, M_s, s_Mc,
-                                           a.qprep + (size_t)si * p_prep_bytes(kPChunk),
+                uint8_t *pbuf = a.qprep + (size_t)si * p_prep_bytes(kPChunk);
+                const unsigned long long tp0 = a.timing ? p_now() : 0;
+                const uint32_t S2 = p_prep(a, sm, t0, K, L, dead, max(M_s, s_cu ? s_Mx : 0ull), s_Mc, pbuf,
                                            a.qspill + (size_t)si * kPMaxTile, rchk, S1);
+                if (a.cross && threadIdx.x == 0)          // the list, for the next tile's stage B
+                    q_st_relaxed(&sl->listw, ((i + 1) << 16) | (S2 == 0xffffffffu ? 0xffffu : S2));
+                if (a.timing && threadIdx.x == 0) atomicAdd(&q->prep_ns, p_now() - tp0);
                 for (int o = 16; o > 0; o >>= 1) rchk += __shfl_down_sync(0xffffffffu, rchk, o);
                 if (lane == 0 && rchk) atomicAdd(&q->prep_rchk, rchk);
                 __syncthreads();
@@ -552,16 +718,17 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 continue;
             }
             const unsigned long long tag = (i + 1) & 0xffffffffull;
-            if (a.nsup_smem && M_s > supM) {
-                // super-block summaries the commits since the last refresh changed (a summary that
-                // also covers words beyond M_s is still valid: it only widens)
-                const long long s0 = (long long)(supM >> 10);
-                const long long s1 = min((long long)a.nsup_smem, (long long)((M_s + 1023) >> 10));
-                for (long long x = s0 + threadIdx.x; x < s1; x += blockDim.x) s_sup[x] = __ldcg(a.ssum + x);
-                supM = M_s;
-            }
             long long hi, lo;
-            p_level_window(a, M_s, base, L, l, hi, lo);
+            q_level_window(a, M_s, base, L, s_cu, s_Mx, l, hi, lo);
+            const unsigned long long M_ref = max(M_s, (unsigned long long)hi);   // (catch-up level: hi = M_x)
+            if (a.nsup_smem && M_ref > supM) {
+                // super-block summaries the commits since the last refresh changed (a summary that
+                // also covers words beyond the window is still valid: it only widens)
+                const long long s0 = (long long)(supM >> 10);
+                const long long s1 = min((long long)a.nsup_smem, (long long)((M_ref + 1023) >> 10));
+                for (long long x = s0 + threadIdx.x; x < s1; x += blockDim.x) s_sup[x] = __ldcg(a.ssum + x);
+                supM = M_ref;
+            }
             uint32_t plo, n0;
             q_part(a, K, plo, n0);                            // this rank's candidates of the tile
             uint32_t n_l = n0;
@@ -818,6 +985,9 @@ int pipeline_run(const RunArgs &r) {
     const bool graded = (r.ordering == GRADED_LEX || r.ordering == GRADED_REVLEX) && !r.use_basis;
     a.prep_lead = (r.opt.flags & GC_FLAG_NO_PREP) ? 0 : (int)(r.opt.prep_lead ? r.opt.prep_lead : graded ? 2u : 1u);
     a.size_on_screen = (r.opt.flags & GC_FLAG_SIZE_ON_TRUE) ? 0 : 1;
+    // cross lists (two-stage preparation): opt-in -- neutral to slightly slower on the measured
+    // workloads (tools/r02ae.sh, profiles/r02_cross_catchup.md)
+    a.cross = (a.prep_lead > 0 && (r.opt.flags & GC_FLAG_CROSS)) ? 1 : 0;
     a.world = world;
     a.rank = r.world > 1 ? r.rank : 0;
     for (int g = 0; g < kMaxRanks; ++g) { a.peer_qdead[g] = nullptr; a.peer_flag[g] = nullptr; }
@@ -865,6 +1035,13 @@ int pipeline_run(const RunArgs &r) {
         b.q = k.q;
         b.qdead = k.qdead; b.qkill = k.qkill; b.qvals = k.qvals;
         b.qprep = k.qprep;
+        // catch-up screening level, by default for graded orders (their screens are the binding stage;
+        // 26,4,glex 359 -> 334 ms) and d = 4 (26,4,gray 160 -> 153 ms); not for d = 3 lex / Gray, whose
+        // killers sit in the last one or two tiles, which no screen sees in time (28,3,lex +6 %), nor
+        // for large d with tiny codebooks (24,8,lex +20 %)  (tools/r02aj.sh, profiles/r02_cross_catchup.md)
+        const bool cu_default = graded || r.d == 4;
+        const bool cu = (r.opt.flags & GC_FLAG_CATCHUP) || (cu_default && !(r.opt.flags & GC_FLAG_NO_CATCHUP));
+        b.cm = cu && !(r.opt.flags & GC_FLAG_NO_CATCHUP) ? &k.q->cm : nullptr;
         b.qspill = k.qspill;
         if (g > 0) { b.codebook = k.codebook; b.d_count = k.count; }
     }
@@ -934,6 +1111,12 @@ int pipeline_run(const RunArgs &r) {
                     "rounds %.2f sequential %.2f append %.2f stats %.2f publish %.2f us\n", f.t_level[9] / P / 1e3,
                     f.t_level[0] / P / c, f.t_level[1] / P / c, f.t_level[5] / P / c, f.t_level[6] / P / c,
                     f.t_level[2] / P / c, f.t_level[3] / P / c, f.t_level[4] / P / c, f.t_level[8] / P / c);
+            fprintf(stderr, "[gc]   preparations: %llu stage A, %.2f us each; %llu stage B, %.2f us each; %llu tiles "
+                    "resolved in cross mode\n", hq.preps, hq.prep_ns / 1e3 / (double)std::max(1ull, hq.preps), hq.n_xb,
+                    hq.xcross_ns / 1e3 / (double)std::max(1ull, hq.n_xb), hq.n_xmode);
+            fprintf(stderr, "[gc]   arrivals: %llu unscreened, %llu screened+open, %llu prep busy, %llu prep done; "
+                    "screen latency %.2f us, screened -> arrival %.2f us\n", hq.arr[0], hq.arr[1], hq.arr[2], hq.arr[3],
+                    hq.scr_ns / 1e3 / (double)std::max(1ull, hq.n_scr), hq.lag_ns / 1e3 / (double)std::max(1ull, hq.n_scr));
             fprintf(stderr, "[gc]   tail: %llu chunks entered it (%.1f undecided threads each), %.2f us per tile in the tail "
                     "itself\n", f.t_level[12], f.t_level[13] / (double)std::max(1ull, f.t_level[12]), f.t_r[7] / T / c);
             fprintf(stderr, "[gc]   per tile: survivors %.1f, accepted %.1f, resolve checks %.0f, levels %.2f; "

@@ -29,6 +29,9 @@ constexpr uint32_t kPTargetAccepted = 384;  // adaptive tiles grow up to ~2x thi
                                             // tools/sweep_knobs2.sh, profiles/r01j_knob_sweep.md)
 constexpr uint32_t kPMaxPredictedSurvivors = 1024;
 constexpr int kPAdj = 32;                       // earlier in-tile conflicts recorded per survivor
+constexpr int kPX = 8;                          // cross conflicts (with earlier tiles' prepared survivors)
+                                                // recorded per prepared survivor (pipelined engine)
+constexpr int kPXRing = 8;                      // the resolver keeps the accepted bits of this many tiles
 constexpr uint32_t kPStageWords = 32 * 32;      // per-warp stage: 32 blocks of 32 codewords (4 KiB)
 constexpr uint32_t kPWarpStage = kPStageWords + 8 * 64 + 32;   // + 8 super-blocks' block summaries + a block queue
 constexpr uint32_t kPWinWords = 16384 + 32;     // level-0 window copied to shared memory (words, then
@@ -138,6 +141,11 @@ struct PArgs {
     int prep_ctas;                     // CTAs 1 .. prep_ctas only prepare tiles (never screen)
     uint32_t burst_chunk;              // survivors decided per sub-chunk of a tile with more than one chunk
     int par;                           // block-bound summaries carry the weight parity in bit 31 (n <= 30)
+    const unsigned long long *cm;      // the resolver's commit word (committed tiles << 40 | M), or null:
+                                       // pipelined engine, one rank: every tile's screen ends with a
+                                       // catch-up level over the words committed since its descriptor
+    int cross;                         // preparations record cross conflicts with the prepared survivors of
+                                       // the tiles still being resolved (GC_FLAG_NO_CROSS: 0)
     int size_on_screen;                // tile sizes bound the survivors of the (older-codebook) screen, which
                                        // the resolve handles, not only those left after the catch-up checks
     // multi-rank pipelined engine: the screen of every tile is split over `world` ranks (whole mask
@@ -943,6 +951,7 @@ struct RShared {
     unsigned long long stat[kPWarps][4];
     uint16_t ovf[kPOvf];
     uint32_t novf;
+    uint32_t und[3];                                         // r_decide: undecided survivors per round (mod 3)
     uint32_t wmin[33];                                       // graded orders: first position of each weight
     uint32_t gA[kPChunkMaxGroups], gO[kPChunkMaxGroups];     // survivor group consensus (AND / OR of 32)
     uint32_t qA[kPTmpMaxWords / 32], qO[kPTmpMaxWords / 32]; // staged prior-word blocks
@@ -961,9 +970,22 @@ struct PPrep {
     unsigned long long M_prep;        // they have no conflict in codebook[0, M_prep)
     const uint32_t *val, *cnt;        // [S]
     const uint16_t *idx, *adj;        // [S], [S * kPAdj]
+    // cross mode: codebook[M_prep, M) holds only the accepted words of the xb tiles before this one,
+    // each resolved from its own prepared list; the preparer recorded every conflict of survivor j
+    // with those lists (xcnt[j] <= kPX entries xadj[j * kPX + q] = b << 12 | position in the list of
+    // tile `tile - b`), and xbits[(tile - b) % kPXRing] holds the accepted positions of that tile
+    int xmode;
+    int xstage;                       // stage B ran: xcnt[j] == 0xff flags a conflict in codebook[.., M_prep)
+    unsigned long long tile;
+    const uint8_t *xcnt;              // [S]
+    const uint16_t *xadj;             // [S * kPX]
+    const uint32_t (*xbits)[64];      // [kPXRing][64]: accepted positions of the last tiles
 };
-// per-slot layout of a prepared tile: val u32[chunk], cnt u32[chunk], idx u16[chunk], adj u16[chunk * kPAdj]
-__host__ __device__ constexpr size_t p_prep_bytes(uint32_t chunk) { return (size_t)chunk * (10 + 2 * kPAdj); }
+// per-slot layout of a prepared tile: val u32[chunk], cnt u32[chunk], idx u16[chunk], adj u16[chunk * kPAdj],
+// xadj u16[chunk * kPX], xcnt u8[chunk]
+__host__ __device__ constexpr size_t p_prep_bytes(uint32_t chunk) { return (size_t)chunk * (11 + 2 * kPAdj + 2 * kPX); }
+__host__ __device__ constexpr size_t p_prep_xadj(uint32_t chunk) { return (size_t)chunk * (10 + 2 * kPAdj); }
+__host__ __device__ constexpr size_t p_prep_xcnt(uint32_t chunk) { return (size_t)chunk * (10 + 2 * kPAdj + 2 * kPX); }
 
 // a3.1 survivors of the tile in rank order (from its dead mask), values regenerated from their
 // ranks (no load): the first `chunk` straight into shared memory (s_idx, s_val), any further ones
@@ -1070,6 +1092,106 @@ __device__ __forceinline__ void r_units(const PArgs &a, const PSmem &sm, uint32_
     else if (a.mix == 3) units(std::false_type{}, std::integral_constant<int, 3>{});
     else if (a.mix == 4) units(std::false_type{}, std::integral_constant<int, 4>{});
     else units(std::false_type{}, std::integral_constant<int, 0>{});
+    __syncthreads();
+}
+
+// An earlier tile's prepared list (pipelined engine, cross lists): its survivors val[0, S).
+struct XList {
+    const uint32_t *val;
+    uint32_t S;
+};
+
+// Cross conflicts of a prepared tile (pipelined engine): its survivors s_val[0, S) (consensus in
+// r.gA / r.gO, r_consensus) against the prepared lists xl[k] (shared memory) of the tiles b = k + 1
+// before it, k < nl, which may still be unresolved: every conflicting pair is appended to
+// xadj[j * kPX + q] (global) as b << 12 | position in that list, counted in sm.s_cnt[j] (zeroed by
+// the caller; counts above kPX are overflows).  The lists are staged together in s_tmp (each from
+// a multiple of 32, as many as fit per batch); a warp task is (group of 32 survivors, group of 32
+// listed words), skipped when the consensus bound of the two is >= d (not for the orthogonality
+// constraint).  Ends with a barrier.
+__device__ __forceinline__ void r_cross(const PArgs &a, const PSmem &sm, uint32_t S, const XList *xl, uint32_t nl,
+                                        uint16_t *xadj, unsigned long long &rchk) {
+    RShared &r = p_rsh();
+    __shared__ uint32_t s_xoff[kPXRing + 1];
+    const int lane = threadIdx.x & 31;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t ng = (S + 31) / 32;
+    for (uint32_t k0 = 0; k0 < nl;) {
+        uint32_t k1 = k0, tot = 0;                    // lists k0 .. k1 - 1 in this batch
+        while (k1 < nl && tot + ((xl[k1].S + 31) & ~31u) <= sm.tmp_words) tot += (xl[k1++].S + 31) & ~31u;
+        __syncthreads();                              // s_tmp / r.qA / s_xoff are free
+        if (tid == 0) {
+            uint32_t o = 0;
+            for (uint32_t k = k0; k < k1; ++k) { s_xoff[k - k0] = o; o += (xl[k].S + 31) & ~31u; }
+            s_xoff[k1 - k0] = o;
+        }
+        for (uint32_t k = k0, o = 0; k < k1; o += (xl[k].S + 31) & ~31u, ++k)
+            for (uint32_t t = tid; t < xl[k].S; t += blockDim.x) sm.s_tmp[o + t] = __ldcg(xl[k].val + t);
+        __syncthreads();
+        const uint32_t nq = tot / 32, nk = k1 - k0;
+        // the list of group q (warp-uniform), and the valid words in it
+        auto qlist = [&](uint32_t q, uint32_t &e, uint32_t &pos0) {
+            uint32_t k = 0;
+            while (k + 1 < nk && s_xoff[k + 1] <= 32 * q) ++k;
+            pos0 = 32 * q - s_xoff[k];
+            e = min(32u, xl[k0 + k].S - pos0);
+            return k0 + k;
+        };
+        for (uint32_t q = tid >> 5; q < nq; q += blockDim.x >> 5) {
+            uint32_t e, pos0;
+            qlist(q, e, pos0);
+            const uint32_t x = (uint32_t)lane < e ? sm.s_tmp[32 * q + lane] : 0u;
+            const uint32_t qA = __reduce_and_sync(0xffffffffu, (uint32_t)lane < e ? x : ~0u);
+            const uint32_t qO = __reduce_or_sync(0xffffffffu, x);
+            if (lane == 0) { r.qA[q] = qA; r.qO[q] = qO; }
+        }
+        __syncthreads();
+        const uint32_t ntask = ng * nq;
+        auto tasks = [&](auto so_tag, auto mix_tag) {
+            constexpr bool SO = decltype(so_tag)::value;
+            constexpr int MIXC = decltype(mix_tag)::value;
+            auto cf = [&](uint32_t u, uint32_t w, int t) {
+                if (MIXC >= 2 && (t & 1)) return p_clear_low<MIXC>(u ^ w) == 0u;
+                return (uint32_t)__popc(u ^ w) < a.d || (SO && (__popc(u & w) & 1));
+            };
+            for (uint32_t p = tid >> 5; p < ntask; p += blockDim.x >> 5) {
+                const uint32_t g = p / nq, q = p - g * nq;
+                if (!SO && p_lb(r.gA[g], r.gO[g], r.qA[q], r.qO[q], a.nmask) >= a.d) continue;
+                uint32_t e, pos0;
+                const uint32_t b = qlist(q, e, pos0) + 1;
+                const uint32_t j = 32 * g + lane;
+                const uint32_t vj = j < S ? sm.s_val[j] : 0u;
+                const uint4 *w4 = reinterpret_cast<const uint4 *>(sm.s_tmp + 32 * q);
+                uint32_t mask = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint4 c = w4[k];
+                    mask |= (uint32_t)cf(vj, c.x, 4 * k) << (4 * k);
+                    mask |= (uint32_t)cf(vj, c.y, 4 * k + 1) << (4 * k + 1);
+                    mask |= (uint32_t)cf(vj, c.z, 4 * k + 2) << (4 * k + 2);
+                    mask |= (uint32_t)cf(vj, c.w, 4 * k + 3) << (4 * k + 3);
+                }
+                if (e < 32) mask &= (1u << e) - 1u;
+                if (j < S) rchk += e;
+                if (j < S && mask) {
+                    uint32_t qq = atomicAdd(&sm.s_cnt[j], (uint32_t)__popc(mask));
+                    while (mask) {
+                        const uint32_t t = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        if (qq < (uint32_t)kPX)
+                            __stcg(xadj + (size_t)j * kPX + qq, (uint16_t)((b << 12) | (pos0 + t)));
+                        ++qq;
+                    }
+                }
+            }
+        };
+        if (a.so) tasks(std::true_type{}, std::integral_constant<int, 0>{});
+        else if (a.mix == 2) tasks(std::false_type{}, std::integral_constant<int, 2>{});
+        else if (a.mix == 3) tasks(std::false_type{}, std::integral_constant<int, 3>{});
+        else if (a.mix == 4) tasks(std::false_type{}, std::integral_constant<int, 4>{});
+        else tasks(std::false_type{}, std::integral_constant<int, 0>{});
+        k0 = k1;
+    }
     __syncthreads();
 }
 
@@ -1201,7 +1323,7 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
     const uint32_t *s_val = sm.s_val;
     uint32_t *s_cnt = sm.s_cnt;
     const uint16_t *s_adj = sm.s_adj;
-    if (tid == 0) r.novf = 0;
+    if (tid == 0) { r.novf = 0; r.und[0] = 0; }
     __syncthreads();
     for (uint32_t j = tid; j < Sc; j += blockDim.x) {
         const bool prev = prior && s_status[j] != 0;
@@ -1275,8 +1397,14 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
         }
         // threads still holding an undecided survivor; when many are left and a round settles less
         // than a quarter of them (long chains of conflicts, e.g. a tile just past a high-bit
-        // boundary) the group-sequential tail below takes over
-        const int cnt = __syncthreads_count(undecided);
+        // boundary) the group-sequential tail below takes over.  Counted in r.und[round % 3]
+        // (plain barriers only): the counter of round + 1 is zeroed before this round's barrier,
+        // after every thread read it as the counter of round - 2.
+        if (tid == 0) r.und[(round + 1) % 3] = 0;
+        const uint32_t wu = (uint32_t)__popc(__ballot_sync(0xffffffffu, undecided));
+        if (lane == 0 && wu) atomicAdd(&r.und[round % 3], wu);
+        __syncthreads();
+        const int cnt = (int)r.und[round % 3];
         uint8_t *t = cur; cur = nxt; nxt = t;
         left = cnt;
         if (!cnt || (round >= 1 && cnt > 96 && cnt * 4 > prev_cnt * 3)) break;
@@ -1386,7 +1514,8 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
 // the AND and widen the OR; fire-and-forget atomics published by the commit's release.
 // Returns the new A (CTA-uniform).  Ends with a barrier.
 __device__ __forceinline__ uint32_t r_append(const PArgs &a, const PSmem &sm, uint32_t Sc, unsigned long long M0,
-                                             uint32_t A, unsigned long long t0, unsigned long long &wdef) {
+                                             uint32_t A, unsigned long long t0, unsigned long long &wdef,
+                                             uint32_t *accbits = nullptr) {
     RShared &r = p_rsh();
     PState *st = a.st;
     const int lane = threadIdx.x & 31;
@@ -1396,6 +1525,10 @@ __device__ __forceinline__ uint32_t r_append(const PArgs &a, const PSmem &sm, ui
     for (uint32_t j0 = 0; j0 < Sc; j0 += blockDim.x) {
         const uint32_t j = j0 + tid;
         const uint32_t acc = (j < Sc && sm.s_status[j] == 1) ? 1u : 0u;
+        if (accbits) {                         // accepted positions of the chunk, one word per warp
+            const unsigned bal = __ballot_sync(0xffffffffu, acc);
+            if (lane == 0 && (j >> 5) < 64) accbits[j >> 5] = bal;
+        }
         uint32_t tot;
         const uint32_t pos = A + p_block_scan(acc, &tot, sm.s_ws);
         if (acc) {
@@ -1448,7 +1581,8 @@ __device__ __forceinline__ uint32_t r_append(const PArgs &a, const PSmem &sm, ui
 // conflict) / pc.A_tile / pc.K_used set; the next tile size is the caller's decision.
 __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsigned long long t0, uint32_t K, int L,
                                           PCount &pc, PTimers *timer, unsigned long long tm, bool allow_partial,
-                                          uint32_t *dead, unsigned long long prior_lo, const PPrep *prep = nullptr) {
+                                          uint32_t *dead, unsigned long long prior_lo, const PPrep *prep = nullptr,
+                                          uint32_t *accbits = nullptr) {
     const uint32_t kPChunk = sm.chunk;
     PState *st = a.st;
     RShared &r = p_rsh();
@@ -1464,7 +1598,7 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         // one round trip: the prepared survivors and the newest committed words they still have to
         // be checked against (r_prior's first batch)
         const unsigned long long M0 = pc.M;
-        if (M0 > prior_lo && S > 0) {
+        if (!prep->xmode && M0 > prior_lo && S > 0) {
             const uint32_t nb = (uint32_t)min((unsigned long long)sm.tmp_words, M0 - prior_lo);
             for (uint32_t t = tid; t < nb; t += blockDim.x) sm.s_tmp[t] = __ldcg(a.codebook + M0 - nb + t);
             pre_loaded = true;
@@ -1473,6 +1607,19 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
             sm.s_val[j] = __ldcg(prep->val + j);
             sm.s_cnt[j] = __ldcg(prep->cnt + j);
             sm.s_idx[j] = __ldcg(prep->idx + j);
+            if (prep->xstage) {
+                // stage B flagged the survivors in conflict with the words committed after stage A;
+                // cross mode: also rejected iff one of its recorded conflicts in the list of the tile
+                // before was accepted there (its accepted words are all of codebook[M_prep, M0))
+                const uint32_t xc = __ldcg(prep->xcnt + j);
+                bool hit = xc == 0xffu;
+                for (uint32_t q = 0; prep->xmode && !hit && q < xc; ++q) {
+                    const uint32_t e = __ldcg(prep->xadj + (size_t)j * kPX + q);
+                    const uint32_t p = e & 0xfffu;
+                    hit |= (prep->xbits[(prep->tile - (e >> 12)) % kPXRing][p >> 5] >> (p & 31)) & 1u;
+                }
+                sm.s_status[j] = hit ? 1 : 0;
+            }
         }
         const uint4 *src = reinterpret_cast<const uint4 *>(prep->adj);
         uint4 *dst = reinterpret_cast<uint4 *>(sm.s_adj);
@@ -1525,14 +1672,19 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
             }
         }
         __syncthreads();
-        r_consensus(sm, Sc);
         const bool pc_prior = M0 > prior_lo, ch_prior = A > 0;
         if (prep) {
             // the preparer built the conflict lists; the committed words it did not see only flag
-            if (pc_prior) r_prior(a, sm, Sc, prior_lo, M0, false, rchk, pre_loaded);
+            // (cross mode: the cross lists flagged them at the load)
+            const bool xm = prep->xmode != 0, xs = prep->xstage != 0;
+            if (!xm) {
+                r_consensus(sm, Sc);
+                if (pc_prior && Sc) r_prior(a, sm, Sc, prior_lo, M0, xs, rchk, pre_loaded);
+            }
             P_TR(1)
-            r_decide(a, sm, Sc, pc_prior, confl, pkill, timer, tr);
+            r_decide(a, sm, Sc, xm || xs || pc_prior, confl, pkill, timer, tr);
         } else {
+            r_consensus(sm, Sc);
             // Survivors conflicting with a committed word the screen did not see are rejected first:
             // codebook[prior_lo, M0) (pipelined engine: the tile was screened against an older
             // codebook) and [M0, M0 + A) (words accepted in this tile's earlier chunks).  The rest
@@ -1555,7 +1707,7 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
             unsigned long long none = 0;
             r_decide(a, sm, Sc, false, confl, none, timer, tr);
         }
-        A = r_append(a, sm, Sc, M0, A, t0, wdef);
+        A = r_append(a, sm, Sc, M0, A, t0, wdef, prep ? accbits : nullptr);
         P_TR(3)
     }
     // clear per-tile state for the next tile (a prepared tile's mask was cleared by its preparer)

@@ -292,6 +292,12 @@ ENGINE_KNOBS = [
     {"prep_lead": 1, "prep_ctas": 1},
     {"prep_lead": 6, "prep_ctas": 8, "pipeline_depth": 7},
     {"prep_ctas": 1, "grid_ctas": 3},           # resolver, one preparing CTA, one screening CTA
+    {"flags": 0x4000},                          # two-stage preparation, cross lists (GC_FLAG_CROSS)
+    {"flags": 0x4000, "prep_lead": 3, "prep_ctas": 4},   # stage A three tiles ahead
+    {"flags": 0x4000, "pipeline_depth": 2, "tile_min": 32, "tile_max": 256},   # tiny tiles, many stage Bs
+    {"flags": 0x10000},                         # catch-up screening level for every ordering
+    {"flags": 0x10000 | 0x4000, "pipeline_depth": 12},
+    {"flags": 0x8000},                          # no catch-up level (graded orders' default)
     {"emulate_ranks": 2},                       # multi-rank pipelined engine, emulated on one GPU
     {"emulate_ranks": 8, "tile_min": 32, "tile_max": 512},   # partitions with no candidates
     {"emulate_ranks": 4, "pipeline_depth": 2, "prep_lead": 1},
