@@ -516,7 +516,8 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 for (int k = 0; k < 8; ++k) t_rp[k] += tmr.r[k] - t_r0[k];
             if (threadIdx.x == 0) {
                 const unsigned long long tp = timer ? clock64() : 0;
-                s_listed[i % kPXRing] = s_mode ? i + 1 : 0;
+                // (a prepared burst decided in sub-chunks has no accepted positions in its list)
+                s_listed[i % kPXRing] = (s_mode && !p_prep_big(a, s_pp)) ? i + 1 : 0;
                 // next descriptor: tile s_issued, screened against the codebook as of now; its
                 // size follows the tile just resolved (p_resolve's pc.K_next)
                 unsigned long long ph = 0, *php = nullptr;

@@ -981,6 +981,11 @@ struct PPrep {
     const uint16_t *xadj;             // [S * kPX]
     const uint32_t (*xbits)[64];      // [kPXRing][64]: accepted positions of the last tiles
 };
+// a prepared tile decided in sub-chunks (p_resolve): more than two sub-chunks of survivors; not after
+// a stage B (its flags only live in the prepared layout)
+__device__ __forceinline__ bool p_prep_big(const PArgs &a, const PPrep &p) {
+    return !p.xstage && p.S > 2u * max(32u, a.burst_chunk);
+}
 // per-slot layout of a prepared tile: val u32[chunk], cnt u32[chunk], idx u16[chunk], adj u16[chunk * kPAdj],
 // xadj u16[chunk * kPX], xcnt u8[chunk]
 __host__ __device__ constexpr size_t p_prep_bytes(uint32_t chunk) { return (size_t)chunk * (11 + 2 * kPAdj + 2 * kPX); }
@@ -1592,7 +1597,15 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
     const unsigned long long tg = timer ? clock64() : 0;
     uint32_t S;
     bool pre_loaded = false;
-    if (prep) {
+    // a prepared burst (more than two sub-chunks of survivors, typically just past a high-bit or a
+    // weight-class boundary, where they conflict densely): decided sub-chunk by sub-chunk from the
+    // prepared list like an unprepared multi-chunk tile -- the words accepted in the earlier sub-chunks
+    // reject most of a later one before its conflict lists are built (the prepared lists are unused)
+    const bool big = prep && p_prep_big(a, *prep);
+    if (big) {
+        S = prep->S;
+        prior_lo = prep->M_prep;
+    } else if (prep) {
         S = prep->S;
         prior_lo = prep->M_prep;
         // one round trip: the prepared survivors and the newest committed words they still have to
@@ -1656,15 +1669,20 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
     // most candidates survive a screen against an older codebook and kill each other): decided in
     // sub-chunks of burst_chunk from a.surv -- each one checked against the words accepted in the
     // earlier ones first, so the in-chunk conflict lists (quadratic) stay small.
-    const bool multi = S > kPChunk;
+    const bool multi = S > kPChunk || big;
     const uint32_t step = multi ? min(kPChunk, max(32u, a.burst_chunk)) : kPChunk;
-    if (multi) {
+    if (multi && !big) {
         for (uint32_t j = tid; j < kPChunk; j += blockDim.x) a.surv[j] = make_uint2(sm.s_idx[j], sm.s_val[j]);
         __syncthreads();
     }
     for (uint32_t c0 = 0; c0 < S; c0 += step) {
         uint32_t Sc = min(step, S - c0);
-        if (multi) {
+        if (big) {
+            for (uint32_t j = tid; j < Sc; j += blockDim.x) {
+                sm.s_idx[j] = __ldcg(prep->idx + c0 + j);
+                sm.s_val[j] = __ldcg(prep->val + c0 + j);
+            }
+        } else if (multi) {
             for (uint32_t j = tid; j < Sc; j += blockDim.x) {
                 const uint2 e = __ldcg(a.surv + c0 + j);
                 sm.s_idx[j] = (uint16_t)e.x;
@@ -1673,7 +1691,7 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         }
         __syncthreads();
         const bool pc_prior = M0 > prior_lo, ch_prior = A > 0;
-        if (prep) {
+        if (prep && !big) {
             // the preparer built the conflict lists; the committed words it did not see only flag
             // (cross mode: the cross lists flagged them at the load)
             const bool xm = prep->xmode != 0, xs = prep->xstage != 0;
@@ -1707,7 +1725,7 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
             unsigned long long none = 0;
             r_decide(a, sm, Sc, false, confl, none, timer, tr);
         }
-        A = r_append(a, sm, Sc, M0, A, t0, wdef, prep ? accbits : nullptr);
+        A = r_append(a, sm, Sc, M0, A, t0, wdef, (prep && !big) ? accbits : nullptr);
         P_TR(3)
     }
     // clear per-tile state for the next tile (a prepared tile's mask was cleared by its preparer)
