@@ -85,13 +85,13 @@ typedef struct gc_options {
     /* persistent engines (development / tuning knobs; 0 = default, none changes the code): */
     uint32_t pipeline_depth; /* pipelined engine: tile i is screened against the codebook committed
                                 after tile i - depth, so `depth` tiles are screened while one is
-                                resolved; 1..16, default 4                                         */
+                                resolved; 1..16, default 8 (graded orders 10)                       */
     uint32_t target_accepted;/* adaptive tiles grow toward ~this many accepted words per tile
                                 (default 384; Gray 768, graded orders 1536)                        */
     uint32_t items_per_warp; /* screen work items per warp and level (default 1; graded orders 4;
                                 2 without the block bound)                                         */
     uint32_t sub_max;        /* longest codeword sub-range of one work item with the block bound,
-                                >= 64 (default 262144)                                             */
+                                >= 64 (default 262144; pipelined engine, graded orders 32768)      */
     uint32_t geo_head;       /* first (newest) sub-range of a level with the block bound; the next
                                 ones double up to sub_max (default 8192)                           */
     uint32_t split_bits;     /* a warp whose live candidates differ in more bits screens them as two
@@ -111,7 +111,8 @@ typedef struct gc_options {
     uint32_t prep_ctas;      /* pipelined engine: CTAs that only prepare tiles (default 2; other
                                 screening CTAs also prepare when idle)                           */
     uint32_t burst_chunk;    /* survivors decided per sub-chunk when a tile has more than one resolve
-                                chunk of them (>= 32, default 512)                               */
+                                chunk of them, or a prepared tile more than two sub-chunks (>= 32,
+                                default 512)                                                     */
 } gc_options;
 
 #define GC_FLAG_NO_EARLY_EXIT  0x1u  /* screen every candidate against the whole codebook, one phase     */

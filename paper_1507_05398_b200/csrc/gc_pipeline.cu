@@ -975,7 +975,12 @@ int pipeline_run(const RunArgs &r) {
     a.tabs = cx->tabs;
     a.vals = nullptr;
     a.dead = nullptr;
-    a.depth = (int)std::min<uint32_t>(r.opt.pipeline_depth ? r.opt.pipeline_depth : 8u, (uint32_t)kQRing);
+    const bool graded = (r.ordering == GRADED_LEX || r.ordering == GRADED_REVLEX) && !r.use_basis;
+    // graded orders: their screens are the binding stage -- sub-ranges of 32768 words per warp item
+    // (more items, shorter ones) and two more tiles in flight (tools/r02am.sh, r02an.sh:
+    // 28,3,glex 2386 -> 1394 ms, 26,4,glex 342 -> 290 ms)
+    a.depth = (int)std::min<uint32_t>(r.opt.pipeline_depth ? r.opt.pipeline_depth : graded ? 10u : 8u, (uint32_t)kQRing);
+    if (graded && !r.opt.sub_max) a.sub_max_bound = 32768u;
     // ranks may run up to 2 x depth tiles apart; a slot is rewritten by a peer only after its
     // previous tile is committed everywhere when 2 x depth < the ring
     if (world > 1) a.depth = std::min(a.depth, kQRing / 2 - 1);
@@ -983,7 +988,6 @@ int pipeline_run(const RunArgs &r) {
     // preparation lead: 1 tile for lex / Gray / B-orders (the resolver then checks only the last
     // tile's words), 2 for graded orders, whose screens are the binding stage and whose preparers
     // need the slack (tools/r02g.sh sweep, profiles/r02g_knob_sweep.log)
-    const bool graded = (r.ordering == GRADED_LEX || r.ordering == GRADED_REVLEX) && !r.use_basis;
     a.prep_lead = (r.opt.flags & GC_FLAG_NO_PREP) ? 0 : (int)(r.opt.prep_lead ? r.opt.prep_lead : graded ? 2u : 1u);
     a.size_on_screen = (r.opt.flags & GC_FLAG_SIZE_ON_TRUE) ? 0 : 1;
     // cross lists (two-stage preparation): opt-in -- neutral to slightly slower on the measured
