@@ -979,8 +979,10 @@ int pipeline_run(const RunArgs &r) {
     // graded orders: their screens are the binding stage -- sub-ranges of 32768 words per warp item
     // (more items, shorter ones) and two more tiles in flight (tools/r02am.sh, r02an.sh:
     // 28,3,glex 2386 -> 1394 ms, 26,4,glex 342 -> 290 ms)
-    a.depth = (int)std::min<uint32_t>(r.opt.pipeline_depth ? r.opt.pipeline_depth : graded ? 10u : 8u, (uint32_t)kQRing);
-    if (graded && !r.opt.sub_max) a.sub_max_bound = 32768u;
+    // (not for constant weight, whose graded scan is one weight class: 24,6,glex,cw=12 26 -> 29 ms)
+    const bool graded_screen = graded && r.constant_weight < 0;
+    a.depth = (int)std::min<uint32_t>(r.opt.pipeline_depth ? r.opt.pipeline_depth : graded_screen ? 10u : 8u, (uint32_t)kQRing);
+    if (graded_screen && !r.opt.sub_max) a.sub_max_bound = 32768u;
     // ranks may run up to 2 x depth tiles apart; a slot is rewritten by a peer only after its
     // previous tile is committed everywhere when 2 x depth < the ring
     if (world > 1) a.depth = std::min(a.depth, kQRing / 2 - 1);
@@ -1044,7 +1046,7 @@ int pipeline_run(const RunArgs &r) {
         // 26,4,glex 359 -> 334 ms) and d = 4 (26,4,gray 160 -> 153 ms); not for d = 3 lex / Gray, whose
         // killers sit in the last one or two tiles, which no screen sees in time (28,3,lex +6 %), nor
         // for large d with tiny codebooks (24,8,lex +20 %)  (tools/r02aj.sh, profiles/r02_cross_catchup.md)
-        const bool cu_default = graded || r.d == 4;
+        const bool cu_default = graded_screen || r.d == 4;
         const bool cu = (r.opt.flags & GC_FLAG_CATCHUP) || (cu_default && !(r.opt.flags & GC_FLAG_NO_CATCHUP));
         b.cm = cu && !(r.opt.flags & GC_FLAG_NO_CATCHUP) ? &k.q->cm : nullptr;
         b.qspill = k.qspill;
