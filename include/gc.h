@@ -154,6 +154,9 @@ typedef struct gc_options {
                                         candidates are screened against the words committed since its
                                         descriptor, so fewer survivors reach the preparation)        */
 #define GC_FLAG_CATCHUP        0x10000u /* pipelined engine: the catch-up level for every ordering          */
+#define GC_FLAG_PIPELINED      0x20000u /* always the pipelined engine (default: d = 3 codes in lexicographic or
+                                        Gray order with n <= 25 run on the tile-barrier engine, which is
+                                        faster there)                                                */
 #define GC_FLAG_KERNEL_TIMING  0x8u  /* bracket every screen launch with CUDA events on the launching
                                         stream; fills gc_stats.screen_ms (benchmarking)               */
 

@@ -34,6 +34,7 @@ GC_FLAG_NO_PARITY_BOUND = 0x2000
 GC_FLAG_CROSS = 0x4000
 GC_FLAG_NO_CATCHUP = 0x8000
 GC_FLAG_CATCHUP = 0x10000
+GC_FLAG_PIPELINED = 0x20000
 GC_FLAG_DEBUG_PHASES = 0x200
 GC_FLAG_NO_SUP_SMEM = 0x400
 

@@ -523,8 +523,16 @@ static int phases_for(unsigned long long M_ub, uint32_t W0, uint32_t growth) {
 
 // ============================================================== host: engine
 
-int engine_run(const RunArgs &a) {
+int engine_run(const RunArgs &a_in) {
     auto wall0 = std::chrono::steady_clock::now();
+    // Engine choice by measurement (profiles/r02ap_knob_engines.log): d = 3 codes in lexicographic
+    // or Gray order up to n = 25 on one rank run on the tile-barrier engine, whose tiles are cut after
+    // 512 survivors (24,3,lex 81 -> 61 ms, 24,3,gray 91 -> 71 ms); from n = 26 the pipelined engine
+    // wins (28,3,lex 590 vs 810 ms).  GC_FLAG_PIPELINED keeps the pipelined engine.
+    RunArgs a = a_in;
+    if (!(a.opt.flags & (GC_FLAG_PIPELINED | GC_FLAG_TILE_BARRIERS)) && a.world <= 1 && a.opt.emulate_ranks <= 1 &&
+        !a.extended() && (a.ordering == GC_LEX || a.ordering == GC_GRAY) && a.d == 3 && a.n <= 25)
+        a.opt.flags |= GC_FLAG_TILE_BARRIERS;
     // default: the pipelined engine (one GPU, emulated ranks, or one rank per GPU with attached
     // peers); then the tile-barrier engines (GC_FLAG_TILE_BARRIERS, or ranks without peers)
     if (pipeline_supported(a)) {

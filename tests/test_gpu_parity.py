@@ -248,7 +248,7 @@ def test_enospc(gc):
         gc.gc_generate_device(10, 3, "lex", cb, cnt, stats=True)
     assert e.value.name == "GC_ENOSPC"
     # without stats: the count reports more than the capacity (never a silently truncated code)
-    for flags in (0, TB):
+    for flags in (PIPELINED, TB):
         cnt.zero_()
         gc.gc_generate_device(10, 3, "lex", cb, cnt, options={"flags": flags})
         torch.cuda.synchronize()
@@ -272,6 +272,7 @@ def test_rank_entry_world1(gc):
 # ------------------------------------------------ engine knobs (gc_options; none changes the code)
 
 TB = 0x100      # GC_FLAG_TILE_BARRIERS: the round-1 tile-synchronous persistent kernel
+PIPELINED = 0x20000   # GC_FLAG_PIPELINED: the pipelined engine even where the tile-barrier one is the default
 
 ENGINE_KNOBS = [
     # pipelined engine (default)
@@ -313,12 +314,26 @@ ENGINE_KNOBS = [
 @pytest.mark.parametrize("knobs", ENGINE_KNOBS, ids=lambda e: "-".join(f"{k}{v}" for k, v in e.items()))
 @pytest.mark.parametrize("n,d,o", [(18, 3, "lex"), (17, 4, "gray"), (16, 3, "glex"), (15, 5, "grlex")])
 def test_engine_knobs_invariance(gc, knobs, n, d, o):
+    knobs = dict(knobs)
+    if not knobs.get("flags", 0) & (TB | 0x10):     # pipelined-engine knobs: keep that engine (d = 3 lex /
+        knobs["flags"] = knobs.get("flags", 0) | PIPELINED   # Gray at n <= 25 default to the tile-barrier one)
     w, st = gpu_code(gc, n, d, o, **knobs)
     assert np.array_equal(w, O.greedy_ball(n, d, o)), knobs
 
 
+@pytest.mark.parametrize("n,d,o", [(18, 3, "lex"), (20, 3, "gray"), (25, 3, "lex")])
+def test_default_engine_choice(gc, n, d, o):
+    # d = 3 lex / Gray with n <= 25 run on the tile-barrier engine by default; both engines agree
+    w1, st1 = gpu_code(gc, n, d, o)
+    w2, st2 = gpu_code(gc, n, d, o, flags=PIPELINED)
+    assert st1["resolve_busy_ms"] == 0 and st2["resolve_busy_ms"] > 0      # which engine ran
+    assert np.array_equal(w1, w2)
+    if n <= 20:
+        assert np.array_equal(w1, O.greedy_ball(n, d, o))
+
+
 def test_pipeline_stats(gc):
-    w, st = gpu_code(gc, 20, 3, "lex")
+    w, st = gpu_code(gc, 20, 3, "lex", flags=PIPELINED)
     assert st["pipeline_depth"] == 8 and st["launches"] == 1 and st["prep_used"] > 0
     assert st["resolve_busy_ms"] > 0 and st["bound_tests"] > 0 and st["checks_exec"] > 0
     w2, st2 = gpu_code(gc, 20, 3, "lex", flags=TB)
