@@ -154,6 +154,10 @@ typedef struct gc_options {
                                         candidates are screened against the words committed since its
                                         descriptor, so fewer survivors reach the preparation)        */
 #define GC_FLAG_CATCHUP        0x10000u /* pipelined engine: the catch-up level for every ordering          */
+#define GC_FLAG_STAGE_B        0x40000u /* pipelined engine: two-stage preparation without cross lists --
+                                        stage A (default 3 tiles ahead) once a tile is screened, stage B
+                                        one tile ahead of the resolver flags the survivors hit by the
+                                        words committed since stage A                               */
 #define GC_FLAG_PIPELINED      0x20000u /* always the pipelined engine (default: d = 3 codes in lexicographic or
                                         Gray order with n <= 25 run on the tile-barrier engine, which is
                                         faster there)                                                */

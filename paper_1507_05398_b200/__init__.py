@@ -27,6 +27,7 @@ from ._binding import (  # noqa: F401
     GC_FLAG_NO_CATCHUP,
     GC_FLAG_CATCHUP,
     GC_FLAG_PIPELINED,
+    GC_FLAG_STAGE_B,
     GC_FLAG_DEBUG_PHASES,
     GC_FLAG_NO_SUP_SMEM,
     GC_B_ORDERING,

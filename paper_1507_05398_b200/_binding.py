@@ -35,6 +35,7 @@ GC_FLAG_CROSS = 0x4000
 GC_FLAG_NO_CATCHUP = 0x8000
 GC_FLAG_CATCHUP = 0x10000
 GC_FLAG_PIPELINED = 0x20000
+GC_FLAG_STAGE_B = 0x40000
 GC_FLAG_DEBUG_PHASES = 0x200
 GC_FLAG_NO_SUP_SMEM = 0x400
 

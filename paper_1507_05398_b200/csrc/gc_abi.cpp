@@ -73,7 +73,7 @@ int resolve_options(const gc_options *opt, Options *out) {
                               GC_FLAG_NO_WEIGHT_BOUND | GC_FLAG_NO_BLOCK_BOUND | GC_FLAG_TILE_BARRIERS |
                               GC_FLAG_DEBUG_PHASES | GC_FLAG_NO_SUP_SMEM | GC_FLAG_NO_PREP |
                               GC_FLAG_SIZE_ON_TRUE | GC_FLAG_NO_PARITY_BOUND | GC_FLAG_CROSS | GC_FLAG_NO_CATCHUP |
-                              GC_FLAG_CATCHUP | GC_FLAG_PIPELINED)) {
+                              GC_FLAG_CATCHUP | GC_FLAG_PIPELINED | GC_FLAG_STAGE_B)) {
         set_error("unknown bits in gc_options.flags");
         return GC_EINVAL;
     }

@@ -130,6 +130,10 @@ __device__ __forceinline__ unsigned long long q_cas_acqrel(unsigned long long *p
     return old;
 }
 
+// Release / acquire fence at GPU scope: every publication in this engine is data stores, this
+// fence, then a relaxed flag store (or atomic), read back with ld.acquire -- the PTX release
+// pattern, which needs no sequentially consistent fence (__threadfence is fence.sc.gpu)
+__device__ __forceinline__ void q_fence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long q_ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -247,7 +251,7 @@ __device__ __forceinline__ unsigned long long q_write(const PArgs &a, QCtl *q, u
 __device__ __forceinline__ void q_finish_level(const PArgs &a, QSlot *sl, unsigned long long i, int l, int L,
                                                uint32_t K, unsigned long long M_s, unsigned long long base,
                                                uint32_t *dead, uint32_t *kill) {
-    __threadfence();                                  // acquire side of the items' release
+    q_fence();                                  // acquire side of the items' release
     const int lane = threadIdx.x & 31;
     uint32_t plo, n0;
     q_part(a, K, plo, n0);
@@ -293,7 +297,7 @@ __device__ __forceinline__ void q_finish_level(const PArgs &a, QSlot *sl, unsign
             sl->nlive[nl] = live;
         }
         if (a.timing && nl >= L) sl->t_scr = p_now();
-        __threadfence();
+        q_fence();
         q_st_relaxed(&sl->phase, ((i + 1) << 8) | (unsigned)nl);
     }
     __syncwarp();
@@ -409,7 +413,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 s_t0[i] = s_next; s_K[i] = K; s_Ms[i] = 0; s_L[i] = 0;
                 q_reset(q, (unsigned long long)i);
                 const unsigned long long ph = q_write(a, q, (unsigned long long)i, s_next, K, 0, 0);
-                __threadfence();
+                q_fence();
                 q_st_relaxed(&q->slot[i].phase, ph);
                 q_flag_empty(a, i, (unsigned long long)i);        // nothing to screen (L == 0)
                 s_next += K;
@@ -479,7 +483,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                                 // accepted words, and the cross lists say which survivors they reject)
                                 const uint32_t xb = q_pw_xb(w);
                                 s_pp.xstage = xb != 0;
-                                const bool xm = xb == 1 && i >= 1 && s_listed[(i - 1) % kPXRing] == i;
+                                const bool xm = a.cross && xb == 1 && i >= 1 && s_listed[(i - 1) % kPXRing] == i;
                                 s_pp.xmode = xm;
                                 if (xm && a.timing) q->n_xmode++;
                                 mode = 1;
@@ -541,7 +545,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 if (pre_reset) in_ahead = q_ld_acquire32(&q->slot[(i + 1 + a.depth) % kQRing].inside);
                 // one fence releases the tile's appended words and summaries (the whole CTA's,
                 // ordered by the barrier at the end of p_resolve) and the new descriptor
-                __threadfence();
+                q_fence();
                 if (php) {
                     q_st_relaxed(php, ph);
                     if ((uint32_t)(ph & 0xff) >= s_L[(int)((s_issued - 1) % kQRing)])   // nothing to screen here
@@ -594,20 +598,22 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                     const unsigned long long cmv = q_ld_acquire(&q->cm);
                     const unsigned long long com = cmv >> 40;
                     // 0. stage B of the tile after the one being resolved (the resolver's next tile)
-                    if (a.cross) {
+                    if (a.stage_b) {
                         const unsigned long long j = com + 1;
                         QSlot *sl = &q->slot[j % kQRing];
                         const unsigned long long w = q_ld_acquire(&sl->prep);
+                        // (only when words were committed since its stage A)
                         if ((w >> 52) == ((j + 1) & 0xfffull) && q_pw_state(w) == kPrepDone && q_pw_xb(w) == 0 &&
-                            q_pw_S(w) != kPrepTooMany && q_pw_S(w) != 0) {
-                            const unsigned long long lw = q_ld_acquire(&q->slot[com % kQRing].listw);
-                            if ((lw >> 16) == com + 1 && (lw & 0xffffu) != 0xffffu) {
+                            q_pw_S(w) != kPrepTooMany && q_pw_S(w) != 0 && __ldcg(&sl->M_s) + q_pw_dM(w) < (cmv & kQM)) {
+                            // cross lists need the list of the tile being resolved
+                            const unsigned long long lw = a.cross ? q_ld_acquire(&q->slot[com % kQRing].listw) : 0ull;
+                            if (!a.cross || ((lw >> 16) == com + 1 && (lw & 0xffffu) != 0xffffu)) {
                                 const unsigned long long wb = (w & ~(3ull << 50)) | ((unsigned long long)kPrepBusy << 50);
                                 if (atomicCAS(&sl->prep, w, wb) == w) {
                                     pick = j;
                                     Mc = cmv & kQM;
                                     c0 = w;
-                                    sprev = (uint32_t)(lw & 0xffffu);
+                                    sprev = a.cross ? (uint32_t)(lw & 0xffffu) : 0u;
                                     lvl = -4;
                                     break;
                                 }
@@ -690,7 +696,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 for (int o = 16; o > 0; o >>= 1) rchk += __shfl_down_sync(0xffffffffu, rchk, o);
                 if (lane == 0 && rchk) atomicAdd(&q->prep_rchk, rchk);
                 if (threadIdx.x == 0) {
-                    __threadfence();
+                    q_fence();
                     // (a CAS: the slot is never rewritten under a stage B, but do not rely on timing)
                     atomicCAS(&sl->prep, (s_wA & ~(3ull << 50)) | ((unsigned long long)kPrepBusy << 50), wn);
                     if (a.timing) { atomicAdd(&q->xcross_ns, p_now() - tp0); atomicAdd(&q->n_xb, 1ull); }
@@ -712,7 +718,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 if (lane == 0 && rchk) atomicAdd(&q->prep_rchk, rchk);
                 __syncthreads();
                 if (threadIdx.x == 0) {
-                    __threadfence();
+                    q_fence();
                     q_st_relaxed(&sl->prep, q_pw(i, kPrepDone, s_Mc - M_s, S2 == 0xffffffffu ? kPrepTooMany : S2, S1));
                     ++n_prep;
                 }
@@ -752,7 +758,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                 c = __shfl_sync(0xffffffffu, c, 0);
                 if ((c >> 32) != tag || (uint32_t)c >= items) break;
                 p_run_item(a, lv, pl.R, (uint32_t)c, C, off, my_checks, my_tests);
-                __threadfence();                              // this item's kills before its arrival
+                q_fence();                              // this item's kills before its arrival
                 __syncwarp();
                 uint32_t dn = 0;
                 if (lane == 0) dn = atomicAdd(&sl->done[l], 1u);
@@ -995,6 +1001,10 @@ int pipeline_run(const RunArgs &r) {
     // cross lists (two-stage preparation): opt-in -- neutral to slightly slower on the measured
     // workloads (tools/r02ae.sh, profiles/r02_cross_catchup.md)
     a.cross = (a.prep_lead > 0 && (r.opt.flags & GC_FLAG_CROSS)) ? 1 : 0;
+    // two-stage preparation: stage A as soon as a tile is screened (prep_lead tiles ahead, default 3),
+    // stage B one tile ahead of the resolver flags the survivors hit by the words committed since
+    a.stage_b = (a.prep_lead > 0 && (a.cross || (r.opt.flags & GC_FLAG_STAGE_B))) ? 1 : 0;
+    if (a.stage_b && !r.opt.prep_lead) a.prep_lead = 3;
     a.world = world;
     a.rank = r.world > 1 ? r.rank : 0;
     for (int g = 0; g < kMaxRanks; ++g) { a.peer_qdead[g] = nullptr; a.peer_flag[g] = nullptr; }

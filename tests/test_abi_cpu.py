@@ -47,7 +47,7 @@ def test_generate_null_pointers_and_bad_options():
     assert B._lib.gc_generate(7, 3, 0, None, None) == 1            # out_count NULL
     assert B._lib.gc_generate(7, 3, 0, None, ctypes.byref(cnt)) == 1   # NULL buffer, capacity 4
     for bad in ({"tile_min": 48}, {"tile_min": 16}, {"tile_max": 1 << 21}, {"tile_min": 1024, "tile_max": 512},
-                {"window0": 1000}, {"emulate_ranks": 3}, {"flags": 0x40000}, {"struct_size": 4},
+                {"window0": 1000}, {"emulate_ranks": 3}, {"flags": 0x80000}, {"struct_size": 4},
                 {"pipeline_depth": 17}, {"sub_max": 32}, {"partial_s": 16}, {"split_bits": 33}, {"prep_lead": 16}):
         opts = {"struct_size": ctypes.sizeof(B.gc_options)}
         opts.update(bad)

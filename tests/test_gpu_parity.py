@@ -299,6 +299,8 @@ ENGINE_KNOBS = [
     {"flags": 0x10000},                         # catch-up screening level for every ordering
     {"flags": 0x10000 | 0x4000, "pipeline_depth": 12},
     {"flags": 0x8000},                          # no catch-up level (graded orders' default)
+    {"flags": 0x40000},                         # two-stage preparation without cross lists (GC_FLAG_STAGE_B)
+    {"flags": 0x40000, "prep_lead": 6, "prep_ctas": 4, "pipeline_depth": 7},
     {"emulate_ranks": 2},                       # multi-rank pipelined engine, emulated on one GPU
     {"emulate_ranks": 8, "tile_min": 32, "tile_max": 512},   # partitions with no candidates
     {"emulate_ranks": 4, "pipeline_depth": 2, "prep_lead": 1},
