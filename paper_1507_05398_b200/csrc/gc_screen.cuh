@@ -949,9 +949,9 @@ struct PSmem {
 
 // Small scratch of the resolve stages (one static shared-memory allocation per kernel).
 struct RShared {
-    unsigned long long stat[kPWarps][4];
     uint16_t ovf[kPOvf];
     uint32_t novf;
+    uint32_t tsum[4];                                        // p_resolve: the tile's counters
     uint32_t und[3];                                         // r_decide: undecided survivors per round (mod 3)
     uint32_t wmin[33];                                       // graded orders: first position of each weight
     uint32_t gA[kPChunkMaxGroups], gO[kPChunkMaxGroups];     // survivor group consensus (AND / OR of 32)
@@ -1520,7 +1520,7 @@ __device__ __forceinline__ void r_decide(const PArgs &a, const PSmem &sm, uint32
 // the AND and widen the OR; fire-and-forget atomics published by the commit's release.
 // Returns the new A (CTA-uniform).  Ends with a barrier.
 __device__ __forceinline__ uint32_t r_append(const PArgs &a, const PSmem &sm, uint32_t Sc, unsigned long long M0,
-                                             uint32_t A, unsigned long long t0, unsigned long long &wdef,
+                                             uint32_t A, unsigned long long t0, unsigned long long &sidx,
                                              uint32_t *accbits = nullptr) {
     RShared &r = p_rsh();
     PState *st = a.st;
@@ -1547,7 +1547,7 @@ __device__ __forceinline__ uint32_t r_append(const PArgs &a, const PSmem &sm, ui
             } else {
                 st->error = 1;
             }
-            if (a.wdef_valid) wdef += a.N - 1 - (t0 + sm.s_idx[j]);
+            sidx += sm.s_idx[j];         // W_def of the tile = A (2^n - 1 - t0) - (sum of in-tile indices)
         }
         A += tot;
     }
@@ -1663,7 +1663,8 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         if (S > kPChunk) atomicAdd(&st->n_chunked, 1ull);
     }
     if (tid < 33) r.wmin[tid] = 0xffffffffu;
-    unsigned long long rchk = 0, confl = 0, wdef = 0, pkill = 0;
+    unsigned long long rchk = 0, confl = 0, sidx = 0, pkill = 0;
+    if (tid < 4) r.tsum[tid] = 0;
     const unsigned long long M0 = pc.M;
     uint32_t A = 0;                   // accepted so far in this tile (codebook[M0, M0+A))
     // More survivors than one chunk (a "burst": e.g. a tile just past a high-bit boundary, where
@@ -1726,36 +1727,34 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
             unsigned long long none = 0;
             r_decide(a, sm, Sc, false, confl, none, timer, tr);
         }
-        A = r_append(a, sm, Sc, M0, A, t0, wdef, (prep && !big) ? accbits : nullptr);
+        A = r_append(a, sm, Sc, M0, A, t0, sidx, (prep && !big) ? accbits : nullptr);
         P_TR(3)
     }
     // clear per-tile state for the next tile (a prepared tile's mask was cleared by its preparer)
     if (!prep)
         for (uint32_t w = tid; w < words; w += blockDim.x) dead[w] = 0;
-    // per-warp reduction, then thread 0 sums the warps' partials (no 64-bit shared atomics,
-    // which are emulated with CAS loops)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        rchk += __shfl_down_sync(0xffffffffu, rchk, o);
-        confl += __shfl_down_sync(0xffffffffu, confl, o);
-        wdef += __shfl_down_sync(0xffffffffu, wdef, o);
-        pkill += __shfl_down_sync(0xffffffffu, pkill, o);
+    // the tile's counters: each fits 32 bits (a tile has < 2^16 candidates, a resolve chunk checks
+    // < 2^12 survivors against < 2^20 words), so one redux.sync per warp and one shared atomic each
+    // replace 64-bit shuffle trees
+    {
+        const uint32_t w0 = __reduce_add_sync(0xffffffffu, (uint32_t)rchk);
+        const uint32_t w1 = __reduce_add_sync(0xffffffffu, (uint32_t)confl);
+        const uint32_t w2 = __reduce_add_sync(0xffffffffu, (uint32_t)sidx);
+        const uint32_t w3 = __reduce_add_sync(0xffffffffu, (uint32_t)pkill);
+        if (lane == 0) {
+            if (w0) atomicAdd(&r.tsum[0], w0);
+            if (w1) atomicAdd(&r.tsum[1], w1);
+            if (w2) atomicAdd(&r.tsum[2], w2);
+            if (w3) atomicAdd(&r.tsum[3], w3);
+        }
     }
-    const int wid = tid >> 5;
-    if (lane == 0) { r.stat[wid][0] = rchk; r.stat[wid][1] = confl; r.stat[wid][2] = wdef; r.stat[wid][3] = pkill; }
     __syncthreads();
     unsigned long long pk = 0;
-    if (wid == 0) {          // warp 0 sums the warps' partials, lane w holding warp w's
-        unsigned long long v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-        if (lane < kPWarps) { v0 = r.stat[lane][0]; v1 = r.stat[lane][1]; v2 = r.stat[lane][2]; v3 = r.stat[lane][3]; }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            v0 += __shfl_down_sync(0xffffffffu, v0, o);
-            v1 += __shfl_down_sync(0xffffffffu, v1, o);
-            v2 += __shfl_down_sync(0xffffffffu, v2, o);
-            v3 += __shfl_down_sync(0xffffffffu, v3, o);
-        }
-        if (lane == 0) { pc.resolve_checks += v0; pc.conflicts += v1; pc.w_def += v2; pk = v3; }
+    if (tid == 0) {
+        pc.resolve_checks += r.tsum[0];
+        pc.conflicts += r.tsum[1];
+        if (a.wdef_valid) pc.w_def += (unsigned long long)A * (a.N - 1 - t0) - r.tsum[2];
+        pk = r.tsum[3];
     }
     if (tid == 0) {
         const uint32_t S_true = S - (uint32_t)min(pk, (unsigned long long)S);
