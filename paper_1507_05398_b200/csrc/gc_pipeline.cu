@@ -134,6 +134,16 @@ __device__ __forceinline__ unsigned long long q_cas_acqrel(unsigned long long *p
 // fence, then a relaxed flag store (or atomic), read back with ld.acquire -- the PTX release
 // pattern, which needs no sequentially consistent fence (__threadfence is fence.sc.gpu)
 __device__ __forceinline__ void q_fence() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long q_ld_relaxed(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned int q_ld_relaxed32(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ unsigned long long q_ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -540,9 +550,11 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                     s_next += Kn;
                     ++s_issued;
                 }
-                // look at the next tile's preparation now: the load's round trip overlaps the fence
-                if (a.prep_lead > 0 && i + 1 < s_issued) w_ahead = q_ld_acquire(&q->slot[(i + 1) % kQRing].prep);
-                if (pre_reset) in_ahead = q_ld_acquire32(&q->slot[(i + 1 + a.depth) % kQRing].inside);
+                // look at the next tile's preparation now: relaxed loads, both in flight at once; the
+                // fence below completes after them and makes them acquires (fence.acq_rel after a
+                // strong read is the PTX acquire pattern)
+                if (a.prep_lead > 0 && i + 1 < s_issued) w_ahead = q_ld_relaxed(&q->slot[(i + 1) % kQRing].prep);
+                if (pre_reset) in_ahead = q_ld_relaxed32(&q->slot[(i + 1 + a.depth) % kQRing].inside);
                 // one fence releases the tile's appended words and summaries (the whole CTA's,
                 // ordered by the barrier at the end of p_resolve) and the new descriptor
                 q_fence();
