@@ -35,6 +35,7 @@ namespace gc {
 
 constexpr int kQRing = kQRingMax;   // tile slots; the pipeline depth D <= kQRing (multi-rank: D <= 7)
 constexpr uint32_t kQChunk = 2048;  // survivors per resolve chunk (and per prepared tile)
+constexpr uint32_t kQScreened = 0x80;   // QSlot::phase: the tile is screened (level field >= L)
 constexpr uint32_t kQWords = kPMaxTile / 32;
 constexpr unsigned long long kQM = (1ull << 40) - 1;   // QCtl::cm: committed tiles << 40 | M
 // watchdog: the resolver gives up (st->error = 2) when one tile's screen, preparation or peer flags
@@ -252,7 +253,7 @@ __device__ __forceinline__ unsigned long long q_write(const PArgs &a, QCtl *q, u
     }
     sl.prep = q_pw(i, kPrepOpen, 0, 0);
     // the phase to open: level 0, or screened when this rank has nothing to screen
-    return ((i + 1) << 8) | (L > 0 && n0 > 0 ? 0u : (uint32_t)L);
+    return ((i + 1) << 8) | (L > 0 && n0 > 0 ? 0u : (kQScreened | (uint32_t)L));
 }
 
 // The warp that finished the last item of level l of tile i: merge the level's kills into the
@@ -308,7 +309,7 @@ __device__ __forceinline__ void q_finish_level(const PArgs &a, QSlot *sl, unsign
         }
         if (a.timing && nl >= L) sl->t_scr = p_now();
         q_fence();
-        q_st_relaxed(&sl->phase, ((i + 1) << 8) | (unsigned)nl);
+        q_st_relaxed(&sl->phase, ((i + 1) << 8) | (nl >= L ? kQScreened : 0u) | (unsigned)nl);
     }
     __syncwarp();
 }
@@ -636,11 +637,14 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                     for (unsigned long long j = com + 1; a.prep_lead > 0 && j <= com + (unsigned long long)a.prep_lead &&
                                                          j < com + (unsigned long long)a.depth; ++j) {
                         QSlot *sl = &q->slot[j % kQRing];
-                        const unsigned long long ph = q_ld_acquire(&sl->phase);
-                        if ((ph >> 8) != j + 1 || (uint32_t)(ph & 0xff) < __ldcg(&sl->L)) continue;
+                        // one round trip: the phase and the prep word together, made acquires by
+                        // the fence (the screened flag of the phase needs no load of L)
+                        const unsigned long long ph = q_ld_relaxed(&sl->phase), pw = q_ld_relaxed(&sl->prep);
+                        q_fence();
+                        if ((ph >> 8) != j + 1 || !(ph & kQScreened)) continue;
                         if (!q_peers_in(a, (int)(j % kQRing), j)) continue;
                         const unsigned long long open = q_pw(j, kPrepOpen, 0, 0);
-                        if (__ldcg(&sl->prep) != open) continue;
+                        if (pw != open) continue;
                         if (atomicCAS(&sl->prep, open, q_pw(j, kPrepBusy, 0, 0)) == open) {
                             pick = j;
                             Mc = cmv & kQM;
@@ -655,8 +659,8 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                         QSlot *sl = &q->slot[i % kQRing];
                         const unsigned long long ph = q_ld_acquire(&sl->phase);
                         if ((ph >> 8) != i + 1) break;           // not published yet
-                        const uint32_t l = (uint32_t)(ph & 0xff);
-                        if (l >= __ldcg(&sl->L)) {                   // screened
+                        const uint32_t l = (uint32_t)(ph & 0x7f);
+                        if (ph & kQScreened) {                       // screened
                             if (i == hint) ++hint;
                             continue;
                         }
