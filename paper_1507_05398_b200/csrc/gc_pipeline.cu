@@ -208,13 +208,14 @@ __device__ __forceinline__ void q_flag_empty(const PArgs &a, int si, unsigned lo
 // CTAs that validated one of its levels may still be about to claim items from it (a claim is an
 // add), so the counters are reset only once none is inside.  Done ahead of time (while waiting
 // for a screen) when the ring is deeper than the pipeline.
-__device__ __forceinline__ void q_reset(QCtl *q, unsigned long long i, unsigned int inside_seen = 1u) {
+// (nlev: the most levels a tile of this run can have, PArgs::reset_levels)
+__device__ __forceinline__ void q_reset(QCtl *q, unsigned long long i, int nlev, unsigned int inside_seen = 1u) {
     QSlot &sl = q->slot[i % kQRing];
     // `inside` of a committed tile's slot only decreases: a 0 read earlier (acquire) stays valid
     if (inside_seen != 0)
         while (q_ld_acquire32(&sl.inside) != 0) __nanosleep(32);
     const unsigned long long tag = (i + 1) & 0xffffffffull;
-    for (int l = 0; l < kPMaxLevels; ++l) { sl.claim[l] = tag << 32; sl.done[l] = 0; }
+    for (int l = 0; l < nlev; ++l) { sl.claim[l] = tag << 32; sl.done[l] = 0; }
 }
 
 // Levels of a tile screened against codebook[base, M_s): the window levels, plus (pipelined engine,
@@ -422,7 +423,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
             for (int i = 0; i < a.depth && s_next < a.t_end; ++i) {
                 const uint32_t K = (uint32_t)min((unsigned long long)a.tile_min, a.t_end - s_next);
                 s_t0[i] = s_next; s_K[i] = K; s_Ms[i] = 0; s_L[i] = 0;
-                q_reset(q, (unsigned long long)i);
+                q_reset(q, (unsigned long long)i, a.reset_levels);
                 const unsigned long long ph = q_write(a, q, (unsigned long long)i, s_next, K, 0, 0);
                 q_fence();
                 q_st_relaxed(&q->slot[i].phase, ph);
@@ -456,7 +457,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                         const unsigned long long ts = __ldcg(&sl->t_scr), tpb = __ldcg(&sl->t_pub);
                         if (scr && ts && tpb && ts > tpb) { q->scr_ns += ts - tpb; q->lag_ns += tw > ts ? tw - ts : 0; q->n_scr++; }
                     }
-                    if (pre_reset && s_next < a.t_end) q_reset(q, i + a.depth, i ? in_ahead : 1u);
+                    if (pre_reset && s_next < a.t_end) q_reset(q, i + a.depth, a.reset_levels, i ? in_ahead : 1u);
                     // Prepared by another CTA?  One CAS: it either hands over the finished preparation
                     // or takes the tile over (nobody started on it: this CTA does all of it).
                     int mode = 0;
@@ -541,7 +542,7 @@ __device__ __forceinline__ void q_body(const PArgs &a, int bid) {
                     if ((unsigned long long)Kn > a.t_end - s_next) Kn = (uint32_t)(a.t_end - s_next);
                     const unsigned long long base = p_base(a, s_next, pc.M);
                     const int sj = (int)(s_issued % kQRing);
-                    if (!pre_reset) q_reset(q, s_issued);
+                    if (!pre_reset) q_reset(q, s_issued, a.reset_levels);
                     s_t0[sj] = s_next; s_K[sj] = Kn; s_Ms[sj] = pc.M;
                     uint32_t cu_;
                     s_L[sj] = (uint32_t)q_levels(a, pc.M, base, cu_);
@@ -1017,6 +1018,17 @@ int pipeline_run(const RunArgs &r) {
     // cross lists (two-stage preparation): opt-in -- neutral to slightly slower on the measured
     // workloads (tools/r02ae.sh, profiles/r02_cross_catchup.md)
     a.cross = (a.prep_lead > 0 && (r.opt.flags & GC_FLAG_CROSS)) ? 1 : 0;
+    {   // the most levels a tile can have: the window levels reaching a full codebook, plus the
+        // catch-up level (q_reset rewrites only these slots' level counters)
+        int L = 0;
+        unsigned long long dsum = 0;
+        while (L < kPMaxLevels && dsum < r.capacity) {
+            const int sh = a.growth * L;
+            dsum += sh >= 40 ? (1ull << 40) : std::min((unsigned long long)a.W0 << sh, 1ull << 40);
+            ++L;
+        }
+        a.reset_levels = std::min(L + 1, kPMaxLevels);
+    }
     // two-stage preparation: stage A as soon as a tile is screened (prep_lead tiles ahead, default 3),
     // stage B one tile ahead of the resolver flags the survivors hit by the words committed since
     a.stage_b = (a.prep_lead > 0 && (a.cross || (r.opt.flags & GC_FLAG_STAGE_B))) ? 1 : 0;

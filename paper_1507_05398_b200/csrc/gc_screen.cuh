@@ -144,6 +144,7 @@ struct PArgs {
     const unsigned long long *cm;      // the resolver's commit word (committed tiles << 40 | M), or null:
                                        // pipelined engine, one rank: every tile's screen ends with a
                                        // catch-up level over the words committed since its descriptor
+    int reset_levels;                  // pipelined engine: level counters reset per slot (levels + catch-up)
     int stage_b;                       // two-stage preparation (GC_FLAG_STAGE_B, or with cross lists)
     int cross;                         // preparations record cross conflicts with the prepared survivors of
                                        // the tiles still being resolved (GC_FLAG_NO_CROSS: 0)
