@@ -1239,9 +1239,11 @@ __device__ __forceinline__ bool r_hit(uint32_t v, const uint32_t *w, uint32_t e,
 // words), skipped when the consensus bound of the two is >= d.  Needs r_consensus.  Ends with a
 // barrier.
 // first_loaded: the newest batch, codebook[hi - min(tmp_words, hi - lo), hi), is already in s_tmp.
+// first_ready (with first_loaded and accumulate): its group consensus is in r.qA / r.qO too and a
+// barrier has passed since -- the first batch's tasks start at once.
 __device__ __forceinline__ void r_prior(const PArgs &a, const PSmem &sm, uint32_t Sc, unsigned long long lo,
                                         unsigned long long hi, bool accumulate, unsigned long long &rchk,
-                                        bool first_loaded = false) {
+                                        bool first_loaded = false, bool first_ready = false) {
     RShared &r = p_rsh();
     const int lane = threadIdx.x & 31;
     const uint32_t tid = threadIdx.x;
@@ -1251,19 +1253,21 @@ __device__ __forceinline__ void r_prior(const PArgs &a, const PSmem &sm, uint32_
     for (unsigned long long top = hi; top > lo;) {
         const uint32_t nb = (uint32_t)min((unsigned long long)sm.tmp_words, top - lo);
         const unsigned long long b0 = top - nb;
-        __syncthreads();
-        if (!first_loaded || top != hi)
-            for (uint32_t t = tid; t < nb; t += blockDim.x) sm.s_tmp[t] = __ldcg(a.codebook + b0 + t);
-        __syncthreads();
         const uint32_t nq = (nb + 31) / 32;
-        for (uint32_t q = tid >> 5; q < nq; q += blockDim.x >> 5) {
-            const uint32_t k = 32 * q + lane;
-            const uint32_t x = k < nb ? sm.s_tmp[k] : 0u;
-            const uint32_t qA = __reduce_and_sync(0xffffffffu, k < nb ? x : ~0u);
-            const uint32_t qO = __reduce_or_sync(0xffffffffu, x);
-            if (lane == 0) { r.qA[q] = qA; r.qO[q] = qO; }
+        if (!(first_ready && top == hi)) {
+            __syncthreads();
+            if (!first_loaded || top != hi)
+                for (uint32_t t = tid; t < nb; t += blockDim.x) sm.s_tmp[t] = __ldcg(a.codebook + b0 + t);
+            __syncthreads();
+            for (uint32_t q = tid >> 5; q < nq; q += blockDim.x >> 5) {
+                const uint32_t k = 32 * q + lane;
+                const uint32_t x = k < nb ? sm.s_tmp[k] : 0u;
+                const uint32_t qA = __reduce_and_sync(0xffffffffu, k < nb ? x : ~0u);
+                const uint32_t qO = __reduce_or_sync(0xffffffffu, x);
+                if (lane == 0) { r.qA[q] = qA; r.qO[q] = qO; }
+            }
+            __syncthreads();
         }
-        __syncthreads();
         const uint32_t ntask = ng * nq;
         auto tasks = [&](auto so_tag, auto mix_tag) {
             constexpr bool SO = decltype(so_tag)::value;
@@ -1613,15 +1617,32 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         // one round trip: the prepared survivors and the newest committed words they still have to
         // be checked against (r_prior's first batch)
         const unsigned long long M0 = pc.M;
+        // the newest words (r_prior's first batch) and the survivors, each 32-group's consensus
+        // (AND / OR) taken by the warp that loads it, statuses initialised: r_consensus and the
+        // first batch of r_prior need no pass and no barrier of their own (pre_ready)
         if (!prep->xmode && M0 > prior_lo && S > 0) {
             const uint32_t nb = (uint32_t)min((unsigned long long)sm.tmp_words, M0 - prior_lo);
-            for (uint32_t t = tid; t < nb; t += blockDim.x) sm.s_tmp[t] = __ldcg(a.codebook + M0 - nb + t);
+            for (uint32_t t0w = 0; t0w < nb; t0w += blockDim.x) {
+                const uint32_t t = t0w + tid;
+                const uint32_t x = t < nb ? __ldcg(a.codebook + M0 - nb + t) : 0u;
+                if (t < nb) sm.s_tmp[t] = x;
+                const uint32_t qA = __reduce_and_sync(0xffffffffu, t < nb ? x : ~0u);
+                const uint32_t qO = __reduce_or_sync(0xffffffffu, x);
+                if (lane == 0 && t < nb) { r.qA[t >> 5] = qA; r.qO[t >> 5] = qO; }
+            }
             pre_loaded = true;
         }
-        for (uint32_t j = tid; j < S; j += blockDim.x) {
-            sm.s_val[j] = __ldcg(prep->val + j);
+        for (uint32_t j0 = 0; j0 < S; j0 += blockDim.x) {
+            const uint32_t j = j0 + tid;
+            const uint32_t x = j < S ? __ldcg(prep->val + j) : 0u;
+            const uint32_t gA = __reduce_and_sync(0xffffffffu, j < S ? x : ~0u);
+            const uint32_t gO = __reduce_or_sync(0xffffffffu, x);
+            if (lane == 0 && j < S) { r.gA[j >> 5] = gA; r.gO[j >> 5] = gO; }
+            if (j >= S) continue;
+            sm.s_val[j] = x;
             sm.s_cnt[j] = __ldcg(prep->cnt + j);
             sm.s_idx[j] = __ldcg(prep->idx + j);
+            if (!prep->xstage) sm.s_status[j] = 0;
             if (prep->xstage) {
                 // stage B flagged the survivors in conflict with the words committed after stage A;
                 // cross mode: also rejected iff one of its recorded conflicts in the list of the tile
@@ -1697,13 +1718,12 @@ __device__ __forceinline__ void p_resolve(const PArgs &a, const PSmem &sm, unsig
         if (prep && !big) {
             // the preparer built the conflict lists; the committed words it did not see only flag
             // (cross mode: the cross lists flagged them at the load)
-            const bool xm = prep->xmode != 0, xs = prep->xstage != 0;
-            if (!xm) {
-                r_consensus(sm, Sc);
-                if (pc_prior && Sc) r_prior(a, sm, Sc, prior_lo, M0, xs, rchk, pre_loaded);
-            }
+            const bool xm = prep->xmode != 0;
+            // (consensus of the survivors and of the newest words taken at the load; statuses zeroed
+            // there, or set from stage B's flags)
+            if (!xm && pc_prior && Sc) r_prior(a, sm, Sc, prior_lo, M0, true, rchk, pre_loaded, pre_loaded);
             P_TR(1)
-            r_decide(a, sm, Sc, xm || xs || pc_prior, confl, pkill, timer, tr);
+            r_decide(a, sm, Sc, xm || prep->xstage || pc_prior, confl, pkill, timer, tr);
         } else {
             r_consensus(sm, Sc);
             // Survivors conflicting with a committed word the screen did not see are rejected first:
