@@ -1032,14 +1032,16 @@ __device__ __forceinline__ uint32_t r_gather(const PArgs &a, const PSmem &sm, un
     return S;
 }
 
-// consensus (AND / OR) of every aligned group of 32 survivors s_val[0, Sc).  Ends with a barrier.
-__device__ __forceinline__ void r_consensus(const PSmem &sm, uint32_t Sc) {
+// consensus (AND / OR) of every aligned group of 32 survivors s_val[0, Sc) (zero_status: their
+// s_status too).  Ends with a barrier.
+__device__ __forceinline__ void r_consensus(const PSmem &sm, uint32_t Sc, bool zero_status = false) {
     RShared &r = p_rsh();
     const int lane = threadIdx.x & 31;
     const uint32_t ng = (Sc + 31) / 32;
     for (uint32_t g = threadIdx.x >> 5; g < ng; g += blockDim.x >> 5) {
         const uint32_t k = 32 * g + lane;
         const uint32_t x = k < Sc ? sm.s_val[k] : 0u;
+        if (zero_status && k < Sc) sm.s_status[k] = 0;
         const uint32_t gA = __reduce_and_sync(0xffffffffu, k < Sc ? x : ~0u);
         const uint32_t gO = __reduce_or_sync(0xffffffffu, x);
         if (lane == 0) { r.gA[g] = gA; r.gO[g] = gO; }
@@ -1820,6 +1822,23 @@ __device__ __forceinline__ uint32_t p_prep(const PArgs &a, const PSmem &sm, unsi
                                            uint32_t *dead, unsigned long long M_s, unsigned long long M_c,
                                            uint8_t *buf, uint2 *spill, unsigned long long &rchk, uint32_t &S_screen) {
     const uint32_t tid = threadIdx.x;
+    // the newest words the survivors are checked against (r_prior's first batch), with their group
+    // consensus, staged while the survivors are gathered (s_tmp is not used by the gather)
+    bool pre = false;
+    if (M_c > M_s) {
+        const int lane = tid & 31;
+        RShared &r = p_rsh();
+        const uint32_t nb = (uint32_t)min((unsigned long long)sm.tmp_words, M_c - M_s);
+        for (uint32_t t0w = 0; t0w < nb; t0w += blockDim.x) {
+            const uint32_t t = t0w + tid;
+            const uint32_t x = t < nb ? __ldcg(a.codebook + M_c - nb + t) : 0u;
+            if (t < nb) sm.s_tmp[t] = x;
+            const uint32_t qA = __reduce_and_sync(0xffffffffu, t < nb ? x : ~0u);
+            const uint32_t qO = __reduce_or_sync(0xffffffffu, x);
+            if (lane == 0 && t < nb) { r.qA[t >> 5] = qA; r.qO[t >> 5] = qO; }
+        }
+        pre = true;
+    }
     const uint32_t S = r_gather(a, sm, t0, K, L, dead, spill);
     S_screen = S;
     uint32_t *val = reinterpret_cast<uint32_t *>(buf);
@@ -1839,8 +1858,8 @@ __device__ __forceinline__ uint32_t p_prep(const PArgs &a, const PSmem &sm, unsi
             __syncthreads();
         }
         if (M_c > M_s && Sc > 0) {
-            r_consensus(sm, Sc);
-            r_prior(a, sm, Sc, M_s, M_c, false, rchk);
+            r_consensus(sm, Sc, true);
+            r_prior(a, sm, Sc, M_s, M_c, true, rchk, pre && c0 == 0, pre && c0 == 0);
             Sc = r_compact(sm, Sc);
         }
         if (out + Sc > sm.chunk) return 0xffffffffu;
