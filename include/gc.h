@@ -87,7 +87,8 @@ typedef struct gc_options {
                                 after tile i - depth, so `depth` tiles are screened while one is
                                 resolved; 1..16, default 8 (graded orders 10)                       */
     uint32_t target_accepted;/* adaptive tiles grow toward ~this many accepted words per tile
-                                (default 384; Gray 768, graded orders 1536)                        */
+                                (default 384; Gray 768 -- 448 on the pipelined engine --, graded
+                                orders 1536)                                                     */
     uint32_t items_per_warp; /* screen work items per warp and level (default 1; graded orders 4;
                                 2 without the block bound)                                         */
     uint32_t sub_max;        /* longest codeword sub-range of one work item with the block bound,

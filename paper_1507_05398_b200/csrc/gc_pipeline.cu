@@ -1006,6 +1006,10 @@ int pipeline_run(const RunArgs &r) {
     const bool graded_screen = graded && r.constant_weight < 0;
     a.depth = (int)std::min<uint32_t>(r.opt.pipeline_depth ? r.opt.pipeline_depth : graded_screen ? 10u : 8u, (uint32_t)kQRing);
     if (graded_screen && !r.opt.sub_max) a.sub_max_bound = 32768u;
+    // Gray order: ~448 accepted words per tile (the tile-barrier engine's 768 leaves the pipelined
+    // resolver and preparation too much per tile: 28,3,gray 602 -> 571 ms, 26,4,gray 150 -> 142.5;
+    // tools/r02bc.sh, profiles/r02bc_knob_target.log)
+    if (r.ordering == GRAY && !r.use_basis && !r.opt.target_accepted) a.target_accepted = 448u;
     // ranks may run up to 2 x depth tiles apart; a slot is rewritten by a peer only after its
     // previous tile is committed everywhere when 2 x depth < the ring
     if (world > 1) a.depth = std::min(a.depth, kQRing / 2 - 1);
